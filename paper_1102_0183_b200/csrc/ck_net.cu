@@ -1,0 +1,933 @@
+// ck_net.cu — the network seam: device-resident nets, the persistent team
+// kernel that runs whole online epochs, batched evaluation, and the C ABI
+// (ck_net_* / ck_committee_*) declared in include/ckb200.h.
+//
+// Replaces, behind the reference's API, NetworkState (network.py:81-304)
+// and the per-image loops of training.train_epoch / evaluate
+// (training.py:126-156).  One launch processes a whole sequence of images:
+// for each image the team runs the phases of PROG_TRAIN (forward, output
+// delta, backward with in-place updates) separated by team barriers.
+#include <cooperative_groups.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "ck_engine.cuh"
+#include "ck_host.h"
+
+namespace ck {
+
+constexpr int kMaxNetsPerLaunch = 64;
+constexpr int kScratchDoubles = 1024;  // output-layer scratch (n_classes <= 1024)
+
+struct NetPtrs {
+  NetDev* p[kMaxNetsPerLaunch];
+};
+
+// ---------------------------------------------------------------------------
+// teams
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct ClusterTeam {
+  __device__ static unsigned rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+  }
+  __device__ static unsigned size() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+  }
+  __device__ static unsigned index(int) {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+  }
+  __device__ static void sync(const NetDev&, int) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+};
+
+struct GridTeam {
+  __device__ static unsigned rank(int ctas) { return blockIdx.x % ctas; }
+  __device__ static unsigned index(int ctas) { return blockIdx.x / ctas; }
+  __device__ static void sync(const NetDev& N, int ctas) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned* count = N.bar;
+      unsigned* gen = N.bar + 1;
+      const unsigned g = ld_acquire(gen);
+      __threadfence();
+      if (atomicAdd(count, 1u) == (unsigned)ctas - 1) {
+        atomicExch(count, 0u);
+        __threadfence();
+        st_release(gen, g + 1);
+      } else {
+        while (ld_acquire(gen) == g) {
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+};
+
+// Copy a net descriptor into shared memory (descriptor reads then never
+// touch L1/L2 inside the image loop).
+__device__ __forceinline__ void load_desc(NetDev* dst, const NetDev* src) {
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(NetDev) / sizeof(int4)); i += blockDim.x) d[i] = s[i];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// persistent training / single-step kernel: one team per net.
+
+template <class Team>
+__global__ void __launch_bounds__(512, 1)
+net_team_kernel(NetPtrs nets, Job job, int ctas) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  NetDev& N = *reinterpret_cast<NetDev*>(smem);
+  double* scratch = reinterpret_cast<double*>(smem + ((sizeof(NetDev) + 15) & ~size_t(15)));
+
+  unsigned rank, team, tsize;
+  if constexpr (std::is_same<Team, ClusterTeam>::value) {
+    rank = ClusterTeam::rank();
+    tsize = ClusterTeam::size();
+    team = ClusterTeam::index(ctas);
+  } else {
+    rank = GridTeam::rank(ctas);
+    tsize = ctas;
+    team = GridTeam::index(ctas);
+  }
+  if ((int)team >= job.n_nets) return;
+  load_desc(&N, nets.p[team]);
+
+  const Program& P = N.prog[job.prog];
+  const int gtid = rank * blockDim.x + threadIdx.x;
+  const int gsize = tsize * blockDim.x;
+  Ctx ctx;
+  ctx.act = N.act;
+  ctx.loss = 0.0;
+  double total = 0.0;
+  for (int64_t t = 0; t < job.n; ++t) {
+    ctx.t = t;
+    ctx.img = job.order ? (int64_t)job.order[t] : job.first + t;
+    ctx.label = job.labels ? job.labels[ctx.img] : -1;
+    for (int ph = 0; ph < P.n_phases; ++ph) {
+      run_phase(N, P, ph, job, ctx, rank, gtid, gsize, scratch);
+      Team::sync(N, ctas);
+    }
+    if (rank == 0 && threadIdx.x == 0 && job.prog != PROG_FORWARD && job.prog != PROG_APPLY) {
+      total += ctx.loss;
+      if (job.losses) job.losses[team * job.n + t] = ctx.loss;
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0 && job.loss_total) job.loss_total[team] = total;
+}
+
+// ---------------------------------------------------------------------------
+// batched evaluation: every CTA is its own team with a private act arena and
+// runs PROG_EVAL on images first+blockIdx.x, first+blockIdx.x+gridDim.x, ...
+// Same per-neuron arithmetic as training's forward, so labels are identical.
+
+__global__ void __launch_bounds__(512)
+net_eval_kernel(const NetDev* net, Job job) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  NetDev& N = *reinterpret_cast<NetDev*>(smem);
+  load_desc(&N, net);
+  const Program& P = N.prog[PROG_EVAL];
+  Ctx ctx;
+  ctx.act = job.eval_scratch + (int64_t)blockIdx.x * N.act_size;
+  const LayerDev& O = N.L[N.n_layers - 1];
+  for (int64_t t = blockIdx.x; t < job.n; t += gridDim.x) {
+    ctx.t = t;
+    ctx.img = job.first + t;
+    for (int ph = 0; ph < P.n_phases; ++ph) {
+      run_phase(N, P, ph, job, ctx, 0, threadIdx.x, blockDim.x, nullptr);
+      __syncthreads();
+    }
+    const float* y = ctx.act + O.y_off;
+    if (threadIdx.x == 0) {
+      // numpy argmax: first maximum; a NaN wins at its first occurrence
+      int best = 0;
+      float bv = y[0];
+      for (int j = 1; j < O.cells && !(bv != bv); ++j) {
+        const float v = y[j];
+        if (v > bv || v != v) { best = j; bv = v; }
+      }
+      job.pred[t] = best;
+    }
+    if (job.outputs)
+      for (int j = threadIdx.x; j < O.cells; j += blockDim.x) job.outputs[t * O.cells + j] = y[j];
+    __syncthreads();
+  }
+}
+
+}  // namespace ck
+
+// ===========================================================================
+// host runtime
+
+using namespace ck;
+
+struct ck_net {
+  int device = 0;
+  NetDev h;                       // host image of the descriptor (device pointers)
+  NetDev* d_desc = nullptr;
+  float* d_params = nullptr;
+  float* d_grads = nullptr;
+  float* d_act = nullptr;
+  int* d_tables = nullptr;
+  double* d_filters = nullptr;
+  unsigned* d_bar = nullptr;
+  double* d_targets = nullptr;    // single-step staging
+  double* d_loss = nullptr;       // per-launch loss total (1 double)
+  float* d_eval = nullptr;        // eval scratch arenas
+  int eval_ctas = 0;
+  int64_t n_params = 0;
+  int team_kind = CK_TEAM_CLUSTER;
+  int team_ctas = 16;
+  int threads = 512;
+  cudaStream_t stream = nullptr;  // private stream for the synchronous calls
+  std::vector<int64_t> grad_count;  // per layer (params it owns)
+};
+
+namespace {
+
+int64_t align32(int64_t v) { return (v + 31) & ~int64_t(31); }
+
+struct ProgramBuilder {
+  Program& p;
+  explicit ProgramBuilder(Program& prog) : p(prog) {
+    memset(&p, 0, sizeof(Program));
+  }
+  int n_ops = 0;
+  std::vector<Op> cur;
+  bool ok = true;
+  void add(int kind, int layer, int flags = 0) {
+    Op o;
+    o.kind = (int16_t)kind;
+    o.layer = (int16_t)layer;
+    o.flags = (int16_t)flags;
+    o.pad = 0;
+    cur.push_back(o);
+  }
+  void phase() {
+    if (cur.empty()) return;
+    if (p.n_phases >= kMaxPhases || n_ops + (int)cur.size() > kMaxOps) {
+      ok = false;
+      cur.clear();
+      return;
+    }
+    p.begin[p.n_phases] = n_ops;
+    for (const Op& o : cur) p.ops[n_ops++] = o;
+    p.n_phases++;
+    p.begin[p.n_phases] = n_ops;
+    cur.clear();
+  }
+};
+
+void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero) {
+  if (load) {
+    b.add(OP_LOAD_INPUT, 0);
+    b.phase();
+  }
+  for (int k = 1; k < N.n_layers; ++k) {
+    const LayerDev& L = N.L[k];
+    const bool scatter_target = zero && k + 1 < N.n_layers &&
+                                N.L[k + 1].kind == L_POOL && L.has_delta;
+    switch (L.kind) {
+      case L_IMGPROC: b.add(OP_IMGPROC, k); break;
+      case L_CONV: b.add(OP_CONV_FWD, k, scatter_target ? F_ZERO_SELF : 0); break;
+      case L_POOL:
+        b.add(OP_POOL_FWD, k);
+        if (scatter_target) b.add(OP_ZERO_DELTA, k);
+        break;
+      case L_FC: b.add(OP_FC_FWD, k); break;
+      default: break;
+    }
+    b.phase();
+  }
+}
+
+// Backward walk of network.py:205-262 as phases.  With `update`, each
+// learnable layer is updated as soon as nothing later reads its old weights:
+// FC rows in place, a conv whose pull is done in the following phase.
+void build_backward(ProgramBuilder& b, const NetDev& N, bool update) {
+  b.add(OP_OUT_DELTA, N.n_layers - 1);
+  b.phase();
+  std::vector<int> pending;
+  int k = N.n_layers - 1;
+  bool done = false;
+  while (!done && k >= 1 && N.L[k].kind == L_FC) {
+    b.add(OP_FC_BWD, k, update ? F_UPDATE : 0);
+    for (int u : pending) b.add(OP_UPDATE, u);
+    pending.clear();
+    b.phase();
+    --k;
+    if (!N.L[k].has_delta) done = true;
+  }
+  while (!done && k >= 1) {
+    const LayerDev& L = N.L[k];
+    if (L.kind == L_CONV) {
+      const bool pull = N.L[k - 1].has_delta;
+      int flags = pull ? F_PULL : 0;
+      if (update && !pull) flags |= F_UPDATE;
+      b.add(OP_CONV_BWD, k, flags);
+      for (int u : pending) b.add(OP_UPDATE, u);
+      pending.clear();
+      b.phase();
+      if (update && pull) pending.push_back(k);
+      if (!pull) break;
+    } else if (L.kind == L_POOL) {
+      if (!N.L[k - 1].has_delta) break;
+    } else {
+      break;
+    }
+    --k;
+  }
+  for (int u : pending) b.add(OP_UPDATE, u);
+  b.phase();
+}
+
+void build_programs(NetDev& N, bool* ok) {
+  {
+    ProgramBuilder b(N.prog[PROG_TRAIN]);
+    build_forward(b, N, true, true);
+    build_backward(b, N, true);
+    *ok = *ok && b.ok;
+  }
+  {
+    ProgramBuilder b(N.prog[PROG_FORWARD]);
+    build_forward(b, N, false, true);
+    *ok = *ok && b.ok;
+  }
+  {
+    ProgramBuilder b(N.prog[PROG_BACKWARD]);
+    build_backward(b, N, false);
+    *ok = *ok && b.ok;
+  }
+  {
+    ProgramBuilder b(N.prog[PROG_APPLY]);
+    for (int k = 1; k < N.n_layers; ++k)
+      if (N.L[k].n_par > 0) b.add(OP_UPDATE, k);
+    b.phase();
+    *ok = *ok && b.ok;
+  }
+  {
+    ProgramBuilder b(N.prog[PROG_EVAL]);
+    build_forward(b, N, true, false);
+    *ok = *ok && b.ok;
+  }
+}
+
+size_t team_smem_bytes() {
+  return ((sizeof(NetDev) + 15) & ~size_t(15)) + kScratchDoubles * sizeof(double);
+}
+
+int configure_kernels() {
+  static bool done = false;
+  if (done) return CK_OK;
+  const int smem = (int)team_smem_bytes();
+  CK_CUDA_TRY(cudaFuncSetAttribute(net_team_kernel<ClusterTeam>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK_CUDA_TRY(cudaFuncSetAttribute(net_team_kernel<ClusterTeam>,
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK_CUDA_TRY(cudaFuncSetAttribute(net_team_kernel<GridTeam>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CK_CUDA_TRY(cudaFuncSetAttribute(net_eval_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(NetDev)));
+  done = true;
+  return CK_OK;
+}
+
+int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
+  int rc = configure_kernels();
+  if (rc) return rc;
+  const ck_net* n0 = nets[0];
+  NetPtrs ptrs;
+  memset(&ptrs, 0, sizeof(ptrs));
+  for (int i = 0; i < n_nets; ++i) {
+    if (nets[i]->team_kind != n0->team_kind || nets[i]->team_ctas != n0->team_ctas ||
+        nets[i]->threads != n0->threads)
+      return set_error(CK_E_CONFIG, "all nets of one launch need the same team config");
+    ptrs.p[i] = nets[i]->d_desc;
+  }
+  job.n_nets = n_nets;
+  const int ctas = n0->team_ctas;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(ctas * n_nets);
+  cfg.blockDim = dim3(n0->threads);
+  cfg.dynamicSmemBytes = team_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (n0->team_kind == CK_TEAM_GRID) {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    e = cudaLaunchKernelEx(&cfg, net_team_kernel<GridTeam>, ptrs, job, ctas);
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    e = cudaLaunchKernelEx(&cfg, net_team_kernel<ClusterTeam>, ptrs, job, ctas);
+  }
+  count_launch();
+  if (e != cudaSuccess) return cuda_status(e, "net_team_kernel launch");
+  return CK_OK;
+}
+
+Job empty_job(int prog) {
+  Job j;
+  memset(&j, 0, sizeof(j));
+  j.prog = prog;
+  j.n = 1;
+  return j;
+}
+
+int run_single(ck_net* net, Job job) {
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  job.loss_total = net->d_loss;
+  int rc = launch_teams(&net, 1, job, net->stream);
+  if (rc) return rc;
+  CK_CUDA_TRY(cudaStreamSynchronize(net->stream));
+  return CK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net** out) {
+  CK_CHECK(layers && out, CK_E_CONFIG, "null argument");
+  CK_CHECK(n_layers >= 2 && n_layers <= kMaxLayers, CK_E_CONFIG, "layer count out of range");
+  CK_CHECK(layers[0].kind == CK_LAYER_INPUT, CK_E_CONFIG, "first layer must be the input");
+  CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG,
+           "last layer must be fully connected (output)");
+  CK_CUDA_TRY(cudaSetDevice(device));
+
+  ck_net* net = new ck_net();
+  net->device = device;
+  NetDev& N = net->h;
+  memset(&N, 0, sizeof(NetDev));
+  N.n_layers = n_layers;
+
+  int64_t p_cursor = 0, a_cursor = 0, t_cursor = 0, f_cursor = 0;
+  std::vector<int64_t> tab_off(n_layers, 0), filt_off(n_layers, 0);
+  for (int k = 0; k < n_layers; ++k) {
+    const ck_layer_desc& D = layers[k];
+    LayerDev& L = N.L[k];
+    L.kind = D.kind;
+    L.maps = D.maps;
+    L.h = D.height;
+    L.w = D.width;
+    if (D.kind == CK_LAYER_FC) L.h = L.w = 1;
+    L.cells = L.maps * L.h * L.w;
+    if (L.maps < 1 || L.h < 1 || L.w < 1) {
+      delete net;
+      return set_error(CK_E_GEOMETRY, "layer " + std::to_string(k) + ": size below 1");
+    }
+    if (k > 0) {
+      const LayerDev& S = N.L[k - 1];
+      L.src_maps = S.maps;
+      L.src_h = S.h;
+      L.src_w = S.w;
+      L.src_cells = S.cells;
+    }
+    L.has_delta = (D.kind == CK_LAYER_CONV || D.kind == CK_LAYER_POOL || D.kind == CK_LAYER_FC);
+    L.y_off = a_cursor;
+    a_cursor = align32(a_cursor + L.cells);
+    if (D.kind == CK_LAYER_CONV || D.kind == CK_LAYER_FC) {
+      L.a_off = a_cursor;
+      a_cursor = align32(a_cursor + L.cells);
+    }
+    if (L.has_delta) {
+      L.d_off = a_cursor;
+      a_cursor = align32(a_cursor + L.cells);
+    }
+    if (D.kind == CK_LAYER_POOL) {
+      L.arg_off = a_cursor;
+      a_cursor = align32(a_cursor + L.cells);
+    }
+    std::string where = "layer " + std::to_string(k) + ": ";
+    switch (D.kind) {
+      case CK_LAYER_INPUT:
+        if (k != 0) { delete net; return set_error(CK_E_CONFIG, where + "input must be first"); }
+        N.in_cells = L.cells;
+        break;
+      case CK_LAYER_IMGPROC:
+        if (k != 1 || D.n_filters < 1 || !D.filter_coeffs || D.filter_h < 1 || D.filter_w < 1 ||
+            D.maps != N.L[0].maps * (1 + D.n_filters) || D.width != N.L[0].w ||
+            D.height != N.L[0].h) {
+          delete net;
+          return set_error(CK_E_CONFIG, where + "bad image-processing layer");
+        }
+        L.n_filt = D.n_filters;
+        L.fh = D.filter_h;
+        L.fw = D.filter_w;
+        filt_off[k] = f_cursor;
+        f_cursor += (int64_t)D.n_filters * D.filter_h * D.filter_w;
+        break;
+      case CK_LAYER_CONV: {
+        const LayerDev& S = N.L[k - 1];
+        if (D.kx < 1 || D.ky < 1 || D.sx < 0 || D.sy < 0 ||
+            (L.h - 1) * (D.sy + 1) + D.ky > S.h || (L.w - 1) * (D.sx + 1) + D.kx > S.w) {
+          delete net;
+          return set_error(CK_E_GEOMETRY, where + "conv geometry does not fit its input");
+        }
+        if (!D.fwd_offsets || !D.fwd_srcs || !D.fwd_widx || !D.bias_offset ||
+            D.arena_size != D.n_pairs * D.kx * D.ky + D.maps) {
+          delete net;
+          return set_error(CK_E_CONFIG, where + "incomplete connection table");
+        }
+        L.kx = D.kx; L.ky = D.ky; L.tx = D.sx + 1; L.ty = D.sy + 1;
+        L.n_pairs = D.n_pairs;
+        L.p_off = p_cursor;
+        L.n_par = D.arena_size;
+        p_cursor += D.arena_size;
+        tab_off[k] = t_cursor;
+        // fwd_off(maps+1) fwd_src fwd_widx bias(maps) bwd_off(src+1) bwd_dst bwd_widx pair_dst
+        t_cursor += (L.maps + 1) + 2 * (int64_t)D.n_pairs + L.maps + (S.maps + 1) +
+                    2 * (int64_t)D.n_pairs + D.n_pairs;
+        break;
+      }
+      case CK_LAYER_POOL: {
+        const LayerDev& S = N.L[k - 1];
+        if (D.px < 1 || D.py < 1 || L.maps != S.maps || L.w != S.w / D.px || L.h != S.h / D.py) {
+          delete net;
+          return set_error(CK_E_GEOMETRY, where + "pool geometry does not match its input");
+        }
+        L.px = D.px; L.py = D.py;
+        break;
+      }
+      case CK_LAYER_FC: {
+        const LayerDev& S = N.L[k - 1];
+        L.p_off = p_cursor;
+        L.b_off = p_cursor + (int64_t)S.cells * L.cells;
+        L.n_par = (int64_t)S.cells * L.cells + L.cells;
+        p_cursor += L.n_par;
+        break;
+      }
+      default:
+        delete net;
+        return set_error(CK_E_CONFIG, where + "unknown layer kind");
+    }
+  }
+  N.n_classes = N.L[n_layers - 1].cells;
+  if (N.n_classes > kScratchDoubles) {
+    delete net;
+    return set_error(CK_E_CONFIG, "too many output classes");
+  }
+  N.act_size = a_cursor;
+  net->n_params = p_cursor;
+
+  // host staging of the int32 tables
+  std::vector<int> tables(std::max<int64_t>(t_cursor, 1));
+  for (int k = 0; k < n_layers; ++k) {
+    if (layers[k].kind != CK_LAYER_CONV) continue;
+    const ck_layer_desc& D = layers[k];
+    const LayerDev& L = N.L[k];
+    const int n_src = N.L[k - 1].maps;
+    int* t = tables.data() + tab_off[k];
+    int* fwd_off = t;           t += L.maps + 1;
+    int* fwd_src = t;           t += D.n_pairs;
+    int* fwd_widx = t;          t += D.n_pairs;
+    int* bias = t;              t += L.maps;
+    int* bwd_off = t;           t += n_src + 1;
+    int* bwd_dst = t;           t += D.n_pairs;
+    int* bwd_widx = t;          t += D.n_pairs;
+    int* pair_dst = t;
+    for (int d = 0; d <= L.maps; ++d) fwd_off[d] = (int)D.fwd_offsets[d];
+    if (fwd_off[L.maps] != D.n_pairs) {
+      delete net;
+      return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": CSR size mismatch");
+    }
+    std::vector<int> count(n_src, 0);
+    for (int p = 0; p < D.n_pairs; ++p) {
+      const int64_t s = D.fwd_srcs[p];
+      if (s < 0 || s >= n_src || D.fwd_widx[p] < 0 ||
+          D.fwd_widx[p] + D.kx * D.ky > D.arena_size) {
+        delete net;
+        return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": table entry out of range");
+      }
+      fwd_src[p] = (int)s;
+      fwd_widx[p] = (int)D.fwd_widx[p];
+      count[s]++;
+    }
+    for (int d = 0; d < L.maps; ++d) {
+      bias[d] = (int)D.bias_offset[d];
+      for (int p = fwd_off[d]; p < fwd_off[d + 1]; ++p) pair_dst[p] = d;
+    }
+    // backward CSR = exact transpose, destinations ascending (topology.invert_table)
+    bwd_off[0] = 0;
+    for (int s = 0; s < n_src; ++s) bwd_off[s + 1] = bwd_off[s] + count[s];
+    std::vector<int> fill(bwd_off, bwd_off + n_src);
+    for (int d = 0; d < L.maps; ++d)
+      for (int p = fwd_off[d]; p < fwd_off[d + 1]; ++p) {
+        const int s = fwd_src[p];
+        bwd_dst[fill[s]] = d;
+        bwd_widx[fill[s]] = fwd_widx[p];
+        fill[s]++;
+      }
+  }
+  std::vector<double> filt(std::max<int64_t>(f_cursor, 1));
+  for (int k = 0; k < n_layers; ++k)
+    if (layers[k].kind == CK_LAYER_IMGPROC)
+      memcpy(filt.data() + filt_off[k], layers[k].filter_coeffs,
+             sizeof(double) * layers[k].n_filters * layers[k].filter_h * layers[k].filter_w);
+
+  bool ok = true;
+  build_programs(N, &ok);
+  if (!ok) {
+    delete net;
+    return set_error(CK_E_CONFIG, "network too deep for the phase program");
+  }
+
+  auto fail = [&](int rc) {
+    ck_net_destroy(net);
+    return rc;
+  };
+  cudaError_t e;
+#define CK_ALLOC(ptr, bytes)                                        \
+  e = cudaMalloc((void**)&(ptr), (bytes));                          \
+  if (e != cudaSuccess) return fail(cuda_status(e, "cudaMalloc"));
+  CK_ALLOC(net->d_desc, sizeof(NetDev));
+  CK_ALLOC(net->d_params, sizeof(float) * std::max<int64_t>(p_cursor, 1));
+  CK_ALLOC(net->d_grads, sizeof(float) * std::max<int64_t>(p_cursor, 1));
+  CK_ALLOC(net->d_act, sizeof(float) * N.act_size);
+  CK_ALLOC(net->d_tables, sizeof(int) * tables.size());
+  CK_ALLOC(net->d_filters, sizeof(double) * filt.size());
+  CK_ALLOC(net->d_bar, 2 * sizeof(unsigned));
+  CK_ALLOC(net->d_targets, sizeof(double) * N.n_classes);
+  CK_ALLOC(net->d_loss, sizeof(double) * 2);
+#undef CK_ALLOC
+  e = cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(cuda_status(e, "cudaStreamCreate"));
+
+  N.params = net->d_params;
+  N.grads = net->d_grads;
+  N.act = net->d_act;
+  N.bar = net->d_bar;
+  for (int k = 0; k < n_layers; ++k) {
+    LayerDev& L = N.L[k];
+    if (L.kind == L_CONV) {
+      int* t = net->d_tables + tab_off[k];
+      const int n_src = N.L[k - 1].maps;
+      L.fwd_off = t;   t += L.maps + 1;
+      L.fwd_src = t;   t += L.n_pairs;
+      L.fwd_widx = t;  t += L.n_pairs;
+      L.bias_off = t;  t += L.maps;
+      L.bwd_off = t;   t += n_src + 1;
+      L.bwd_dst = t;   t += L.n_pairs;
+      L.bwd_widx = t;  t += L.n_pairs;
+      L.pair_dst = t;
+    }
+    if (L.kind == L_IMGPROC) L.filt = net->d_filters + filt_off[k];
+  }
+  e = cudaMemcpy(net->d_tables, tables.data(), sizeof(int) * tables.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(cuda_status(e, "upload tables"));
+  e = cudaMemcpy(net->d_filters, filt.data(), sizeof(double) * filt.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(cuda_status(e, "upload filters"));
+  e = cudaMemcpy(net->d_desc, &N, sizeof(NetDev), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return fail(cuda_status(e, "upload descriptor"));
+  e = cudaMemset(net->d_bar, 0, 2 * sizeof(unsigned));
+  if (e != cudaSuccess) return fail(cuda_status(e, "zero barrier"));
+  e = cudaMemset(net->d_act, 0, sizeof(float) * N.act_size);
+  if (e != cudaSuccess) return fail(cuda_status(e, "zero activations"));
+  e = cudaMemset(net->d_grads, 0, sizeof(float) * std::max<int64_t>(p_cursor, 1));
+  if (e != cudaSuccess) return fail(cuda_status(e, "zero grads"));
+  *out = net;
+  return CK_OK;
+}
+
+int ck_net_destroy(ck_net* net) {
+  if (!net) return CK_OK;
+  cudaSetDevice(net->device);
+  if (net->stream) cudaStreamDestroy(net->stream);
+  cudaFree(net->d_desc);
+  cudaFree(net->d_params);
+  cudaFree(net->d_grads);
+  cudaFree(net->d_act);
+  cudaFree(net->d_tables);
+  cudaFree(net->d_filters);
+  cudaFree(net->d_bar);
+  cudaFree(net->d_targets);
+  cudaFree(net->d_loss);
+  cudaFree(net->d_eval);
+  delete net;
+  return CK_OK;
+}
+
+int ck_net_set_team(ck_net* net, int kind, int ctas, int threads) {
+  CK_CHECK(net, CK_E_CONFIG, "null net");
+  if (kind == CK_TEAM_AUTO) kind = CK_TEAM_CLUSTER;
+  CK_CHECK(kind == CK_TEAM_CLUSTER || kind == CK_TEAM_GRID, CK_E_CONFIG, "unknown team kind");
+  CK_CHECK(threads >= 32 && threads <= 512 && threads % 32 == 0, CK_E_CONFIG,
+           "threads must be a multiple of 32 in [32, 512]");
+  CK_CHECK(ctas >= 1 && (kind == CK_TEAM_GRID || ctas <= 16), CK_E_CONFIG,
+           "cluster teams hold 1..16 CTAs");
+  net->team_kind = kind;
+  net->team_ctas = ctas;
+  net->threads = threads;
+  return CK_OK;
+}
+
+int ck_net_get_team(const ck_net* net, int* kind, int* ctas, int* threads) {
+  CK_CHECK(net && kind && ctas && threads, CK_E_CONFIG, "null argument");
+  *kind = net->team_kind;
+  *ctas = net->team_ctas;
+  *threads = net->threads;
+  return CK_OK;
+}
+
+int ck_net_num_params(const ck_net* net, int64_t* n) {
+  CK_CHECK(net && n, CK_E_CONFIG, "null argument");
+  *n = net->n_params;
+  return CK_OK;
+}
+
+int ck_net_set_params(ck_net* net, const float* host, int64_t n) {
+  CK_CHECK(net && host, CK_E_CONFIG, "null argument");
+  CK_CHECK(n == net->n_params, CK_E_DIMENSION, "parameter count mismatch");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  CK_CUDA_TRY(cudaMemcpy(net->d_params, host, sizeof(float) * n, cudaMemcpyHostToDevice));
+  return CK_OK;
+}
+
+int ck_net_get_params(ck_net* net, float* host, int64_t n) {
+  CK_CHECK(net && host, CK_E_CONFIG, "null argument");
+  CK_CHECK(n == net->n_params, CK_E_DIMENSION, "parameter count mismatch");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  CK_CUDA_TRY(cudaMemcpy(host, net->d_params, sizeof(float) * n, cudaMemcpyDeviceToHost));
+  return CK_OK;
+}
+
+static int stage_input(ck_net* net, const float* x) {
+  const LayerDev& I = net->h.L[0];
+  CK_CUDA_TRY(cudaMemcpyAsync(net->d_act + I.y_off, x, sizeof(float) * I.cells,
+                              cudaMemcpyHostToDevice, net->stream));
+  return CK_OK;
+}
+
+int ck_net_forward(ck_net* net, const float* x, float* y_out) {
+  CK_CHECK(net && x, CK_E_CONFIG, "null argument");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  int rc = stage_input(net, x);
+  if (rc) return rc;
+  Job job = empty_job(PROG_FORWARD);
+  rc = run_single(net, job);
+  if (rc) return rc;
+  if (y_out) {
+    const LayerDev& O = net->h.L[net->h.n_layers - 1];
+    CK_CUDA_TRY(cudaMemcpy(y_out, net->d_act + O.y_off, sizeof(float) * O.cells,
+                           cudaMemcpyDeviceToHost));
+  }
+  return CK_OK;
+}
+
+int ck_net_backward(ck_net* net, const double* targets) {
+  CK_CHECK(net && targets, CK_E_CONFIG, "null argument");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  CK_CUDA_TRY(cudaMemcpyAsync(net->d_targets, targets, sizeof(double) * net->h.n_classes,
+                              cudaMemcpyHostToDevice, net->stream));
+  Job job = empty_job(PROG_BACKWARD);
+  job.targets = net->d_targets;
+  return run_single(net, job);
+}
+
+int ck_net_apply_gradients(ck_net* net, double eta) {
+  CK_CHECK(net, CK_E_CONFIG, "null net");
+  CK_CHECK(eta > 0, CK_E_CONFIG, "learning rate must be > 0");
+  Job job = empty_job(PROG_APPLY);
+  job.eta_f = (float)eta;
+  return run_single(net, job);
+}
+
+int ck_net_train_step(ck_net* net, const float* x, const double* targets, double eta,
+                      double* loss) {
+  CK_CHECK(net && x && targets, CK_E_CONFIG, "null argument");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  int rc = stage_input(net, x);
+  if (rc) return rc;
+  CK_CUDA_TRY(cudaMemcpyAsync(net->d_targets, targets, sizeof(double) * net->h.n_classes,
+                              cudaMemcpyHostToDevice, net->stream));
+  // eta <= 0: forward + loss + gradients without an update (network.py:279-281)
+  Job job = empty_job(eta > 0 ? PROG_TRAIN : PROG_BACKWARD);
+  if (eta <= 0) {
+    Job fwd = empty_job(PROG_FORWARD);
+    rc = run_single(net, fwd);
+    if (rc) return rc;
+  }
+  job.targets = net->d_targets;
+  job.eta_f = (float)eta;
+  rc = run_single(net, job);
+  if (rc) return rc;
+  if (loss) CK_CUDA_TRY(cudaMemcpy(loss, net->d_loss, sizeof(double), cudaMemcpyDeviceToHost));
+  return CK_OK;
+}
+
+int ck_net_buffer_size(const ck_net* net, int layer, int which, int64_t* count) {
+  CK_CHECK(net && count, CK_E_CONFIG, "null argument");
+  CK_CHECK(layer >= 0 && layer < net->h.n_layers, CK_E_DIMENSION, "layer out of range");
+  const LayerDev& L = net->h.L[layer];
+  switch (which) {
+    case CK_BUF_Y: *count = L.cells; return CK_OK;
+    case CK_BUF_A:
+      CK_CHECK(L.kind == L_CONV || L.kind == L_FC, CK_E_STATE, "layer has no pre-activations");
+      *count = L.cells; return CK_OK;
+    case CK_BUF_DELTA:
+      CK_CHECK(L.has_delta, CK_E_STATE, "layer keeps no deltas");
+      *count = L.cells; return CK_OK;
+    case CK_BUF_ARG:
+      CK_CHECK(L.kind == L_POOL, CK_E_STATE, "layer has no pool index");
+      *count = L.cells; return CK_OK;
+    case CK_BUF_GRAD:
+      CK_CHECK(L.n_par > 0, CK_E_STATE, "layer has no parameters");
+      *count = L.n_par; return CK_OK;
+    default: return set_error(CK_E_CONFIG, "unknown buffer");
+  }
+}
+
+int ck_net_read_buffer(ck_net* net, int layer, int which, void* host, int64_t count) {
+  int64_t n = 0;
+  int rc = ck_net_buffer_size(net, layer, which, &n);
+  if (rc) return rc;
+  CK_CHECK(host && count == n, CK_E_DIMENSION, "buffer size mismatch");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  const LayerDev& L = net->h.L[layer];
+  const void* src = nullptr;
+  switch (which) {
+    case CK_BUF_Y: src = net->d_act + L.y_off; break;
+    case CK_BUF_A: src = net->d_act + L.a_off; break;
+    case CK_BUF_DELTA: src = net->d_act + L.d_off; break;
+    case CK_BUF_ARG: src = net->d_act + L.arg_off; break;
+    case CK_BUF_GRAD: src = net->d_grads + L.p_off; break;
+  }
+  CK_CUDA_TRY(cudaMemcpy(host, src, 4 * n, cudaMemcpyDeviceToHost));
+  return CK_OK;
+}
+
+int ck_committee_train_epoch(ck_net* const* nets, int n_nets, const uint8_t* images,
+                             const float* lut, const int32_t* labels, const int32_t* order,
+                             int64_t n, double eta, double* mean_losses, ck_stream_t stream) {
+  CK_CHECK(nets && n_nets >= 1 && n_nets <= kMaxNetsPerLaunch, CK_E_CONFIG,
+           "need 1..64 nets");
+  CK_CHECK(images && labels, CK_E_CONFIG, "null dataset pointer");
+  CK_CHECK(n >= 1, CK_E_CONFIG, "empty epoch");
+  CK_CHECK(eta > 0, CK_E_CONFIG, "learning rate must be > 0");
+  for (int i = 0; i < n_nets; ++i) {
+    CK_CHECK(nets[i] && nets[i]->device == nets[0]->device, CK_E_CONFIG,
+             "committee nets must live on one device");
+    CK_CHECK(nets[i]->h.in_cells == nets[0]->h.in_cells, CK_E_DIMENSION,
+             "committee nets must share the input geometry");
+  }
+  CK_CUDA_TRY(cudaSetDevice(nets[0]->device));
+  double* d_tot = nullptr;
+  CK_CUDA_TRY(cudaMallocAsync((void**)&d_tot, sizeof(double) * n_nets, (cudaStream_t)stream));
+  Job job = empty_job(PROG_TRAIN);
+  job.images = images;
+  job.lut = lut;
+  job.labels = labels;
+  job.order = order;
+  job.n = n;
+  job.first = 0;
+  job.eta_f = (float)eta;
+  job.loss_total = d_tot;
+  int rc = launch_teams(nets, n_nets, job, (cudaStream_t)stream);
+  if (rc == CK_OK && mean_losses) {
+    std::vector<double> tot(n_nets);
+    cudaError_t e = cudaMemcpyAsync(tot.data(), d_tot, sizeof(double) * n_nets,
+                                    cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) rc = cuda_status(e, "read losses");
+    for (int i = 0; i < n_nets && rc == CK_OK; ++i) mean_losses[i] = tot[i] / (double)n;
+  }
+  cudaFreeAsync(d_tot, (cudaStream_t)stream);
+  return rc;
+}
+
+int ck_net_train_epoch(ck_net* net, const uint8_t* images, const float* lut,
+                       const int32_t* labels, const int32_t* order, int64_t n, double eta,
+                       double* losses, double* mean_loss, ck_stream_t stream) {
+  CK_CHECK(net, CK_E_CONFIG, "null net");
+  if (!losses) return ck_committee_train_epoch(&net, 1, images, lut, labels, order, n, eta,
+                                               mean_loss, stream);
+  CK_CHECK(images && labels, CK_E_CONFIG, "null dataset pointer");
+  CK_CHECK(n >= 1, CK_E_CONFIG, "empty epoch");
+  CK_CHECK(eta > 0, CK_E_CONFIG, "learning rate must be > 0");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  Job job = empty_job(PROG_TRAIN);
+  job.images = images;
+  job.lut = lut;
+  job.labels = labels;
+  job.order = order;
+  job.n = n;
+  job.eta_f = (float)eta;
+  job.losses = losses;
+  job.loss_total = net->d_loss;
+  int rc = launch_teams(&net, 1, job, (cudaStream_t)stream);
+  if (rc) return rc;
+  if (mean_loss) {
+    double tot = 0;
+    CK_CUDA_TRY(cudaMemcpyAsync(&tot, net->d_loss, sizeof(double), cudaMemcpyDeviceToHost,
+                                (cudaStream_t)stream));
+    CK_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    *mean_loss = tot / (double)n;
+  }
+  return CK_OK;
+}
+
+int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut, int64_t first,
+                int64_t n, int32_t* pred, float* outputs, ck_stream_t stream) {
+  CK_CHECK(net && images && pred, CK_E_CONFIG, "null argument");
+  CK_CHECK(n >= 0 && first >= 0, CK_E_CONFIG, "bad image range");
+  if (n == 0) return CK_OK;
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  int rc = configure_kernels();
+  if (rc) return rc;
+  int sms = 148;
+  CK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device));
+  const int ctas = (int)std::min<int64_t>(n, (int64_t)sms * 2);
+  if (ctas > net->eval_ctas) {
+    CK_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    cudaFree(net->d_eval);
+    net->d_eval = nullptr;
+    net->eval_ctas = 0;
+    CK_CUDA_TRY(cudaMalloc((void**)&net->d_eval, sizeof(float) * net->h.act_size * ctas));
+    net->eval_ctas = ctas;
+  }
+  Job job = empty_job(PROG_EVAL);
+  job.images = images;
+  job.lut = lut;
+  job.first = first;
+  job.n = n;
+  job.pred = pred;
+  job.outputs = outputs;
+  job.eval_scratch = net->d_eval;
+  net_eval_kernel<<<ctas, 256, sizeof(NetDev), (cudaStream_t)stream>>>(net->d_desc, job);
+  count_launch();
+  CK_CUDA_TRY(cudaGetLastError());
+  return CK_OK;
+}
+
+}  // extern "C"

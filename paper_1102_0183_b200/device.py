@@ -1,0 +1,61 @@
+"""Device plumbing (PyTorch is used only for memory and streams).
+
+Datasets are uploaded once per (dataset, device) as uint8 (n, C, H, W) plus
+the 256-entry normalisation LUT and int32 labels; the CUDA engine reads them
+in place for every epoch and every evaluation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .data import Dataset, byte_lut
+from .errors import StateError
+
+
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise StateError("no CUDA device is visible (the engine has no CPU fallback)")
+    return torch
+
+
+def current_stream_handle(device: int = 0) -> int:
+    torch = torch_cuda()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class DeviceDataset:
+    """Resident copy of a Dataset on one GPU."""
+
+    def __init__(self, data: Dataset, device: int = 0):
+        torch = torch_cuda()
+        dev = torch.device("cuda", device)
+        self.n = len(data)
+        self.device = device
+        self.in_shape = (data.channels, data.height, data.width)
+        if data.raw is not None:
+            self.images = torch.from_numpy(np.ascontiguousarray(data.raw)).to(dev)
+            self.lut = torch.from_numpy(byte_lut()).to(dev)
+        else:   # arbitrary float32 inputs: the engine reads them directly
+            self.images = torch.from_numpy(
+                np.ascontiguousarray(data.images, dtype=np.float32)).to(dev)
+            self.lut = None
+        self.labels = torch.from_numpy(np.ascontiguousarray(data.labels, np.int32)).to(dev)
+
+    @property
+    def images_ptr(self) -> int:
+        return self.images.data_ptr()
+
+    @property
+    def lut_ptr(self) -> int | None:
+        return None if self.lut is None else self.lut.data_ptr()
+
+
+def device_dataset(data: Dataset, device: int = 0) -> DeviceDataset:
+    cache = getattr(data, "_device_cache", None)
+    if cache is None:
+        return DeviceDataset(data, device)
+    if device not in cache:
+        cache[device] = DeviceDataset(data, device)
+    return cache[device]
