@@ -162,7 +162,8 @@ int ck_net_train_step(ck_net* net, const float* x, const double* targets,
 
 /* Inspection of a layer's buffers after the last call (dense, unpitched):
  * which = CK_BUF_A | CK_BUF_Y | CK_BUF_DELTA (float32), CK_BUF_ARG (int32
- * flat source index r*src_w+c), CK_BUF_GRAD (float32 arena / FC W then b). */
+ * index of the winner in the whole source layer, m*src_h*src_w + r*src_w + c),
+ * CK_BUF_GRAD (float32 arena / FC W then b). */
 enum { CK_BUF_A = 0, CK_BUF_Y = 1, CK_BUF_DELTA = 2, CK_BUF_ARG = 3, CK_BUF_GRAD = 4 };
 int ck_net_buffer_size(const ck_net* net, int layer, int which, int64_t* count);
 int ck_net_read_buffer(ck_net* net, int layer, int which, void* host, int64_t count);
@@ -192,6 +193,17 @@ int ck_committee_train_epoch(ck_net* const* nets, int n_nets,
 int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut,
                 int64_t first, int64_t n, int32_t* pred, float* outputs,
                 ck_stream_t stream);
+
+/* Instrumented PROG_TRAIN run over n images: average device time of every
+ * phase (team barrier to team barrier, %globaltimer ns) into phase_ns. */
+int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
+                         const int32_t* labels, const int32_t* order, int64_t n,
+                         double eta, int64_t* phase_ns, int max_phases,
+                         int* n_phases);
+
+/* Human-readable phase program (0 train, 1 forward, 2 backward, 3 apply,
+ * 4 eval) for diagnostics and DESIGN.md. */
+int ck_net_describe_program(const ck_net* net, int prog, char* buf, int cap);
 
 #ifdef __cplusplus
 }

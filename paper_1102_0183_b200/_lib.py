@@ -80,6 +80,9 @@ _SIGNATURES = {
     "ck_committee_train_epoch": (_i32, [C.POINTER(_vp), _i32, _vp, _vp, _vp, _vp, _i64,
                                         _f64, C.POINTER(_f64), _vp]),
     "ck_net_eval": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "ck_net_profile_epoch": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _f64, _vp, _i32,
+                                    C.POINTER(_i32)]),
+    "ck_net_describe_program": (_i32, [_vp, _i32, C.c_char_p, _i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -5,14 +5,20 @@
 //           reference's tiling topology.py:82-96, FC W (n_in,n_out), FC b)
 //   grads   f32, same layout (backward() / apply_gradients() split mode)
 //   act     per layer y / a / delta (f32, dense (maps,h,w), no pitch) and pool
-//           argmax (int32 flat source index), 128-byte aligned
+//           argmax (int32 index into the source layer), 128-byte aligned
 //   tables  int32 copies of the ConnectionTable CSR arrays
 //
 // One online step is a PROGRAM: a list of phases, each a list of ops that may
 // run concurrently; phases are separated by a team barrier.  A team is the
 // set of CTAs working on one net (a thread-block cluster, a cooperative grid
-// or a single CTA for batched evaluation).  All ops distribute their work
-// over the team's threads (gtid, gsize) and never need a barrier inside.
+// or a single CTA for batched evaluation).  Ops split their work over the
+// team's CTAs / warps / threads; within a CTA they may stage data in shared
+// memory (with __syncthreads), never across CTAs.
+//
+// Every reduction whose order is free (the reference accumulates it in f64)
+// is split in a way that depends only on fixed constants (warp width, group
+// sizes, FC slices), never on the launch shape, so results are identical for
+// every team shape and between training and evaluation.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -24,6 +30,8 @@ namespace ck {
 constexpr int kMaxLayers = 24;
 constexpr int kMaxOps = 80;
 constexpr int kMaxPhases = 56;
+constexpr int kFcSlices = 16;      // FC forward: i-slices combined in fixed order
+constexpr int kPullLanes = 8;      // pull: lanes per source cell
 
 enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
 
@@ -36,6 +44,7 @@ struct LayerDev {
   int n_pairs;
   int has_delta;
   int n_filt, fh, fw;              // imgproc
+  int max_fan_in;                  // conv: largest forward row
   int64_t p_off, b_off, n_par;     // params: conv arena / FC W, FC bias, count
   int64_t y_off, a_off, d_off, arg_off;  // act arena offsets (elements)
   const int* fwd_off;              // conv tables (device, int32)
@@ -52,7 +61,7 @@ struct LayerDev {
 enum OpKind {
   OP_LOAD_INPUT = 0,  // input y <- lut[image bytes] (no-op for host-staged x)
   OP_IMGPROC,         // contrast layer
-  OP_CONV_FWD,        // conv a, y (+ zero own delta when aux & 1)
+  OP_CONV_FWD,        // conv a, y (+ zero own delta with F_ZERO_SELF)
   OP_POOL_FWD,        // max-pool y + argmax
   OP_FC_FWD,          // a = x@W + b, y = act(a)
   OP_ZERO_DELTA,      // delta <- 0 (scatter target of the pool above)
@@ -60,6 +69,7 @@ enum OpKind {
   OP_FC_BWD,          // xgrad, W/b update (or grads), delta below
   OP_CONV_BWD,        // weight/bias grads (+ update) and pulled delta below
   OP_UPDATE,          // params[p_off, +n_par) -= eta * grads
+  OP_FC_OUT,          // output layer: forward + output deltas + loss + backward rows
 };
 
 enum OpFlags { F_UPDATE = 1, F_PULL = 2, F_ZERO_SELF = 4 };
@@ -111,6 +121,8 @@ struct Job {
   int32_t* pred;           // eval
   float* outputs;          // eval (nullable)
   float* eval_scratch;     // eval: per-CTA act arenas
+  long long* prof;         // phase end times (globaltimer ns), nullable
+  int64_t prof_images;     // images profiled
 };
 
 struct Ctx {
@@ -120,6 +132,32 @@ struct Ctx {
   int label;
   double loss;             // written by OP_OUT_DELTA (valid in its thread)
 };
+
+// Where this thread sits in its team, plus the CTA's shared scratch.
+struct TeamCtx {
+  int rank, size;          // CTA rank in the team / CTAs in the team
+  int gtid, gsize;         // thread index / count over the team
+  int gwarp, gwarps;       // warp index / count over the team
+  float* smem;             // per-CTA scratch
+  int smem_floats;
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Work split: items [0, n) are cut into one contiguous, balanced range per
+// CTA of the team; threads (or warps) stride inside their CTA's range.
+struct Span {
+  int b, e;
+};
+__device__ __forceinline__ Span cta_span(int64_t n, const TeamCtx& tm) {
+  return Span{(int)(n * tm.rank / tm.size), (int)(n * (tm.rank + 1) / tm.size)};
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // delta routing: `v` is the gathered (pre-derivative) delta of cell `cell` in
@@ -146,93 +184,182 @@ __device__ __forceinline__ void emit_delta(const NetDev& N, float* act, int s,
 }
 
 // ---------------------------------------------------------------------------
-// ops
+// input and contrast layer
 
 __device__ __forceinline__ void op_load_input(const NetDev& N, const Job& job,
-                                              const Ctx& ctx, int gtid, int gsize) {
+                                              const Ctx& ctx, const TeamCtx& tm) {
   if (!job.images) return;
   float* y = ctx.act + N.L[0].y_off;
   if (job.lut) {
     const uint8_t* img = job.images + ctx.img * (int64_t)N.in_cells;
-    for (int i = gtid; i < N.in_cells; i += gsize) y[i] = job.lut[img[i]];
+    const Span sp = cta_span(N.in_cells, tm);
+    for (int i = sp.b + threadIdx.x; i < sp.e; i += blockDim.x) y[i] = job.lut[img[i]];
   } else {  // float32 dataset
     const float* img = reinterpret_cast<const float*>(job.images) + ctx.img * (int64_t)N.in_cells;
-    for (int i = gtid; i < N.in_cells; i += gsize) y[i] = img[i];
+    const Span sp = cta_span(N.in_cells, tm);
+    for (int i = sp.b + threadIdx.x; i < sp.e; i += blockDim.x) y[i] = img[i];
   }
 }
 
-__device__ __forceinline__ void op_imgproc(const NetDev& N, const LayerDev& L,
-                                           float* act, int gtid, int gsize) {
+// correlate(mode="nearest") per (filter, channel): f64 sum, one rounding.
+// One warp per output cell: lanes split the taps, fixed-order xor reduction.
+__device__ __forceinline__ void op_imgproc(const NetDev& N, const LayerDev& L, float* act,
+                                           const TeamCtx& tm) {
   const LayerDev& I = N.L[0];
   const float* src = act + I.y_off;
   float* out = act + L.y_off;
   const int hw = L.h * L.w;
   const int C = I.maps;
+  const Span cp = cta_span(C * hw, tm);
+  for (int q = cp.b + threadIdx.x; q < cp.e; q += blockDim.x) out[q] = src[q];
   const int cy = L.fh / 2, cx = L.fw / 2;
-  for (int q = gtid; q < L.cells; q += gsize) {
+  const int taps = L.fh * L.fw;
+  const int lane = lane_id();
+  const int n_resp = L.cells - C * hw;
+  const Span rs = cta_span(n_resp, tm);
+  for (int r = rs.b + (threadIdx.x >> 5); r < rs.e; r += blockDim.x >> 5) {
+    const int q = C * hw + r;
     const int o = q / hw, pix = q % hw;
-    if (o < C) { out[q] = src[q]; continue; }
     const int y = pix / L.w, x = pix % L.w;
     const int f = (o - C) / C, c = (o - C) % C;
     const float* s = src + c * hw;
-    const double* k = L.filt + (int64_t)f * L.fh * L.fw;
+    const double* k = L.filt + (int64_t)f * taps;
     double acc = 0.0;
-    for (int i = 0; i < L.fh; ++i) {
-      const float* row = s + min(max(y + i - cy, 0), L.h - 1) * L.w;
-      for (int j = 0; j < L.fw; ++j)
-        acc = __dadd_rn(acc, __dmul_rn(k[i * L.fw + j], (double)row[min(max(x + j - cx, 0), L.w - 1)]));
+    for (int t = lane; t < taps; t += 32) {
+      const int i = t / L.fw, j = t % L.fw;
+      const int yy = min(max(y + i - cy, 0), L.h - 1);
+      const int xx = min(max(x + j - cx, 0), L.w - 1);
+      acc = __dadd_rn(acc, __dmul_rn(k[t], (double)s[yy * L.w + xx]));
     }
-    out[q] = (float)acc;
+    acc = warp_sum(acc);
+    if (lane == 0) out[q] = (float)acc;
   }
 }
 
-__device__ __forceinline__ void op_conv_fwd(const NetDev& N, const LayerDev& L, int flags,
-                                            float* act, int gtid, int gsize) {
+// ---------------------------------------------------------------------------
+// conv forward (kernels.py:70-87)
+
+// One output cell, reference order: bias, then per connected source k, rows
+// v, columns u; every product and sum rounded to f32 separately.
+template <int KX, int KY>
+__device__ __forceinline__ float conv_cell(float acc, const float* src, const int* soff,
+                                           const float* w, int nk, int sw, int kx, int ky) {
+  if constexpr (KX > 0) {
+    for (int k = 0; k < nk; ++k) {
+      const float* s = src + soff[k];
+      const float* wk = w + k * (KX * KY);
+      float xs[KX * KY];
+#pragma unroll
+      for (int v = 0; v < KY; ++v)
+#pragma unroll
+        for (int u = 0; u < KX; ++u) xs[v * KX + u] = s[v * sw + u];
+#pragma unroll
+      for (int t = 0; t < KX * KY; ++t) acc = __fadd_rn(acc, __fmul_rn(wk[t], xs[t]));
+    }
+  } else {
+    const int kk = kx * ky;
+    for (int k = 0; k < nk; ++k) {
+      const float* s = src + soff[k];
+      const float* wk = w + k * kk;
+      for (int v = 0; v < ky; ++v)
+        for (int u = 0; u < kx; ++u) acc = __fadd_rn(acc, __fmul_rn(wk[v * kx + u], s[v * sw + u]));
+    }
+  }
+  return acc;
+}
+
+// The team's cells are split into one contiguous chunk per CTA.  The chunk's
+// weights (contiguous in the arena: per dest [blocks..., bias]) and source
+// map offsets are staged in shared memory; the source layer too when it fits.
+template <int KX, int KY>
+__device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, float* act,
+                               const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
-  const float* src = act + S.y_off;
+  const int hw = L.h * L.w;
+  const int64_t Q = (int64_t)L.cells;
+  const int q0 = (int)(Q * tm.rank / tm.size);
+  const int q1 = (int)(Q * (tm.rank + 1) / tm.size);
+  if (q0 >= q1) return;
+  const int d0 = q0 / hw, d1 = (q1 - 1) / hw;
+  const int kk = L.kx * L.ky;
+  const int k0 = L.fwd_off[d0], k1 = L.fwd_off[d1 + 1];
   const float* arena = N.params + L.p_off;
+  const int w0 = L.fwd_widx[k0];                      // first weight of map d0
+  const int n_w = L.bias_off[d1] + 1 - w0;            // through d1's bias
+  const int n_src = S.cells;
+
+  // shared layout: [src offsets (k1-k0 ints)] [weights n_w] [source layer]
+  int* soff = reinterpret_cast<int*>(tm.smem);
+  float* ws = tm.smem + (k1 - k0);
+  float* ss = ws + n_w;
+  const bool w_in_smem = (k1 - k0) + n_w <= tm.smem_floats;
+  const bool s_in_smem = w_in_smem && (k1 - k0) + n_w + n_src <= tm.smem_floats;
+  const float* src_g = act + S.y_off;
+  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = L.fwd_src[k0 + k] * (S.h * S.w);
+  if (w_in_smem)
+    for (int i = threadIdx.x; i < n_w; i += blockDim.x) ws[i] = arena[w0 + i];
+  if (s_in_smem)
+    for (int i = threadIdx.x; i < n_src; i += blockDim.x) ss[i] = src_g[i];
+  __syncthreads();
+  const float* wbase = w_in_smem ? ws : arena + w0;
+  const float* sbase = s_in_smem ? ss : src_g;
+  const int* offs = w_in_smem ? soff : nullptr;
+
   float* a = act + L.a_off;
   float* y = act + L.y_off;
   float* dl = act + L.d_off;
-  const int hw = L.h * L.w;
-  const int shw = S.h * S.w;
-  const int kx = L.kx, ky = L.ky;
-  for (int q = gtid; q < L.cells; q += gsize) {
+  for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const int d = q / hw, pix = q % hw;
     const int r = pix / L.w, c = pix % L.w;
-    float acc = arena[L.bias_off[d]];
-    const int k1 = L.fwd_off[d + 1];
-    for (int k = L.fwd_off[d]; k < k1; ++k) {
-      const float* s = src + L.fwd_src[k] * shw + (r * L.ty) * S.w + c * L.tx;
-      const float* w = arena + L.fwd_widx[k];
-      for (int v = 0; v < ky; ++v)
-        for (int u = 0; u < kx; ++u)
-          acc = __fadd_rn(acc, __fmul_rn(w[v * kx + u], s[v * S.w + u]));
+    const int kb = L.fwd_off[d], ke = L.fwd_off[d + 1];
+    const float* w = wbase + (L.fwd_widx[kb] - w0);
+    float acc = w[(ke - kb) * kk];                    // bias slot follows the blocks
+    const int rc = (r * L.ty) * S.w + c * L.tx;
+    if (offs) {
+      acc = conv_cell<KX, KY>(acc, sbase + rc, offs + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+    } else {
+      for (int k = kb; k < ke; ++k) {
+        const int so = L.fwd_src[k] * (S.h * S.w);
+        acc = conv_cell<KX, KY>(acc, sbase + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
+      }
     }
     a[q] = acc;
     y[q] = conv_act(acc);
     if (flags & F_ZERO_SELF) dl[q] = 0.0f;
   }
+  __syncthreads();
 }
 
-__device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L,
-                                            float* act, int gtid, int gsize) {
+__device__ __forceinline__ void op_conv_fwd(const NetDev& N, const LayerDev& L, int flags,
+                                            float* act, const TeamCtx& tm) {
+  if (L.kx == 2 && L.ky == 2) conv_fwd_chunk<2, 2>(N, L, flags, act, tm);
+  else if (L.kx == 3 && L.ky == 3) conv_fwd_chunk<3, 3>(N, L, flags, act, tm);
+  else if (L.kx == 4 && L.ky == 4) conv_fwd_chunk<4, 4>(N, L, flags, act, tm);
+  else if (L.kx == 5 && L.ky == 5) conv_fwd_chunk<5, 5>(N, L, flags, act, tm);
+  else conv_fwd_chunk<0, 0>(N, L, flags, act, tm);
+}
+
+// max-pool (kernels.py:154-172): strict '>' keeps the first cell in scan order.
+// The argmax is stored as an index into the whole source layer.
+__device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L, float* act,
+                                            const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
   const float* src = act + S.y_off;
   float* y = act + L.y_off;
   int* arg = reinterpret_cast<int*>(act + L.arg_off);
   const int hw = L.h * L.w;
   const int shw = S.h * S.w;
-  for (int q = gtid; q < L.cells; q += gsize) {
+  const Span sp = cta_span(L.cells, tm);
+  for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) {
     const int m = q / hw, pix = q % hw;
     const int r = pix / L.w, c = pix % L.w;
-    const float* s = src + m * shw;
-    int best_i = (r * L.py) * S.w + c * L.px;
-    float best = s[best_i];
+    const int base = m * shw;
+    int best_i = base + (r * L.py) * S.w + c * L.px;
+    float best = src[best_i];
     for (int v = 0; v < L.py; ++v)
       for (int u = 0; u < L.px; ++u) {
-        const int i = (r * L.py + v) * S.w + c * L.px + u;
-        const float val = s[i];
+        const int i = base + (r * L.py + v) * S.w + c * L.px + u;
+        const float val = src[i];
         if (val > best) { best = val; best_i = i; }
       }
     y[q] = best;
@@ -240,27 +367,78 @@ __device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L,
   }
 }
 
-__device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L,
-                                          float* act, int gtid, int gsize) {
-  const LayerDev& S = N.L[&L - N.L - 1];
-  const float* x = act + S.y_off;
-  const float* W = N.params + L.p_off;
-  const float* b = N.params + L.b_off;
-  const int n_in = S.cells, n_out = L.cells;
-  for (int j = gtid; j < n_out; j += gsize) {
-    double acc = 0.0;
-    for (int i = 0; i < n_in; ++i)
-      acc = fma((double)x[i], (double)W[(int64_t)i * n_out + j], acc);
-    const float aj = __fadd_rn((float)acc, b[j]);
-    act[L.a_off + j] = aj;
-    act[L.y_off + j] = fc_act(aj);
+// ---------------------------------------------------------------------------
+// shared-memory staging helper: copy n floats into the CTA's scratch when
+// they fit, else keep reading global memory (the caller __syncthreads()).
+__device__ __forceinline__ const float* stage(const float* src, int n, const TeamCtx& tm,
+                                              int& used) {
+  if (used + n > tm.smem_floats) return src;
+  float* dst = tm.smem + used;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const int n4 = n >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) d4[i] = s4[i];
+    for (int i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
   }
+  used += (n + 3) & ~3;
+  return dst;
 }
 
-__device__ __forceinline__ void op_zero_delta(const LayerDev& L, float* act, int gtid,
-                                              int gsize) {
+// ---------------------------------------------------------------------------
+// FC forward (network.py:193-199).  One 32-column tile: lanes own columns,
+// the n_in rows are cut into kFcSlices interleaved slices (warps), and the
+// f64 partials are combined in slice order — independent of launch shape.
+// Returns a_j (valid in warp 0 for j < n_out); all threads must call.
+__device__ __forceinline__ float fc_tile_preact(const float* x, const float* W, const float* b,
+                                                int n_in, int n_out, int tile, double* red) {
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int j = tile * 32 + lane;
+  for (int sl = warp; sl < kFcSlices; sl += nwarps) {
+    double part = 0.0;
+    if (j < n_out)
+      for (int i = sl; i < n_in; i += kFcSlices)
+        part = fma((double)x[i], (double)W[(int64_t)i * n_out + j], part);
+    red[sl * 32 + lane] = part;
+  }
+  __syncthreads();
+  float aj = 0.0f;
+  if (warp == 0 && j < n_out) {
+    double acc = 0.0;
+    for (int sl = 0; sl < kFcSlices; ++sl) acc += red[sl * 32 + lane];
+    aj = __fadd_rn((float)acc, b[j]);
+  }
+  __syncthreads();
+  return aj;
+}
+
+__device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, float* act,
+                                          const TeamCtx& tm) {
+  const LayerDev& S = N.L[&L - N.L - 1];
+  const int n_tiles = (L.cells + 31) / 32;
+  if (tm.rank >= n_tiles) return;
+  int used = 0;
+  const float* x = stage(act + S.y_off, S.cells, tm, used);
+  double* red = reinterpret_cast<double*>(tm.smem + used);   // [kFcSlices][32]
+  __syncthreads();
+  for (int tile = tm.rank; tile < n_tiles; tile += tm.size) {
+    const float aj = fc_tile_preact(x, N.params + L.p_off, N.params + L.b_off, S.cells, L.cells,
+                                    tile, red);
+    const int j = tile * 32 + lane_id();
+    if ((threadIdx.x >> 5) == 0 && j < L.cells) {
+      act[L.a_off + j] = aj;
+      act[L.y_off + j] = fc_act(aj);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void op_zero_delta(const LayerDev& L, float* act, const TeamCtx& tm) {
   float* d = act + L.d_off;
-  for (int q = gtid; q < L.cells; q += gsize) d[q] = 0.0f;
+  const Span sp = cta_span(L.cells, tm);
+  for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) d[q] = 0.0f;
 }
 
 // Output deltas (backprop.py:22-32) and the sample loss (backprop.py:35-39):
@@ -269,7 +447,7 @@ __device__ __forceinline__ void op_out_delta(const NetDev& N, const Job& job, Ct
                                              double* scratch) {
   const LayerDev& L = N.L[N.n_layers - 1];
   const int n = L.cells;
-  const int lane = threadIdx.x & 31;
+  const int lane = lane_id();
   for (int j = lane; j < n; j += 32) {
     const float yj = ctx.act[L.y_off + j];
     const double t = job.targets ? job.targets[j] : (j == ctx.label ? 1.0 : -1.0);
@@ -282,33 +460,26 @@ __device__ __forceinline__ void op_out_delta(const NetDev& N, const Job& job, Ct
   __syncwarp();
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// FC backward, one warp per input row i (network.py:213-230): the row of W
-// is read once for xgrad_i = sum_j W[i,j] delta_j and then updated in place
-// with grad_w[i,j] = f32(x_i * delta_j) (or stored as a gradient).
-__device__ __forceinline__ void op_fc_bwd(const NetDev& N, const LayerDev& L, int flags,
-                                          float eta_f, float* act, int gtid, int gsize) {
-  const int li = &L - N.L;
+// FC backward rows (network.py:213-230), one warp per input row i: the row
+// of W is read once for xgrad_i = sum_j W[i,j] delta_j (f64) and then
+// updated in place with grad_w[i,j] = f32(x_i * delta_j) (or stored).
+__device__ __forceinline__ void fc_bwd_rows(const NetDev& N, const LayerDev& L, int li,
+                                           int flags, float eta_f, float* act, const float* x,
+                                           const float* dl, const TeamCtx& tm) {
   const LayerDev& S = N.L[li - 1];
-  const float* x = act + S.y_off;
-  const float* dl = act + L.d_off;
   float* W = N.params + L.p_off;
   float* b = N.params + L.b_off;
   float* gW = N.grads + L.p_off;
   float* gb = N.grads + L.b_off;
   const int n_in = S.cells, n_out = L.cells;
   const bool upd = flags & F_UPDATE;
-  const int lane = gtid & 31;
-  for (int j = gtid; j < n_out; j += gsize) {
+  const int lane = lane_id();
+  for (int j = tm.gtid; j < n_out; j += tm.gsize) {
     if (upd) b[j] = sgd(b[j], eta_f, dl[j]);
     else gb[j] = dl[j];
   }
-  for (int i = gtid >> 5; i < n_in; i += gsize >> 5) {
+  const Span rows = cta_span(n_in, tm);
+  for (int i = rows.b + (threadIdx.x >> 5); i < rows.e; i += blockDim.x >> 5) {
     float* row = W + (int64_t)i * n_out;
     double acc = 0.0;
     for (int j = lane; j < n_out; j += 32) acc = fma((double)row[j], (double)dl[j], acc);
@@ -323,101 +494,245 @@ __device__ __forceinline__ void op_fc_bwd(const NetDev& N, const LayerDev& L, in
   }
 }
 
-// Conv backward (network.py:233-252): weight_grad (kernels.py:124-141),
-// bias_grad (kernels.py:144-151) and, when the layer below keeps deltas,
-// pull_bwd (kernels.py:90-121) routed through emit_delta.  With F_UPDATE the
-// weights are updated in place (legal only without F_PULL: pull reads them).
-__device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, int flags,
-                                            float eta_f, float* act, int gtid, int gsize) {
+__device__ __forceinline__ void op_fc_bwd(const NetDev& N, const LayerDev& L, int flags,
+                                          float eta_f, float* act, const TeamCtx& tm) {
+  const int li = &L - N.L;
+  fc_bwd_rows(N, L, li, flags, eta_f, act, act + N.L[li - 1].y_off, act + L.d_off, tm);
+}
+
+// The output layer in one phase: every CTA recomputes the output layer's
+// forward (a tiny n_in x n_classes product) and the output deltas in its own
+// shared memory, rank 0 publishes a / y / delta and the loss, then all CTAs
+// run the FC backward rows.  Replaces three barrier-separated phases.
+__device__ __forceinline__ void op_fc_out(const NetDev& N, const LayerDev& L, int flags,
+                                          const Job& job, Ctx& ctx, const TeamCtx& tm,
+                                          double* scratch) {
   const int li = &L - N.L;
   const LayerDev& S = N.L[li - 1];
-  const float* dl = act + L.d_off;
-  const float* ys = act + S.y_off;
+  float* act = ctx.act;
+  int used = 0;
+  const float* x = stage(act + S.y_off, S.cells, tm, used);
+  float* yd = tm.smem + used;                    // [a | y | delta] x n_out
+  used += (3 * L.cells + 3) & ~3;
+  double* red = reinterpret_cast<double*>(tm.smem + used);
+  __syncthreads();
+  const int n_tiles = (L.cells + 31) / 32;
+  for (int tile = 0; tile < n_tiles; ++tile) {
+    const float aj = fc_tile_preact(x, N.params + L.p_off, N.params + L.b_off, S.cells, L.cells,
+                                    tile, red);
+    const int j = tile * 32 + lane_id();
+    if ((threadIdx.x >> 5) == 0 && j < L.cells) {
+      yd[j] = aj;
+      yd[L.cells + j] = fc_act(aj);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int n = L.cells, lane = lane_id();
+    for (int j = lane; j < n; j += 32) {
+      const double t = job.targets ? job.targets[j] : (j == ctx.label ? 1.0 : -1.0);
+      const double r = (double)yd[n + j] - t;
+      yd[2 * n + j] = (float)(r * (double)act_deriv(yd[j]));
+      scratch[j] = r * r;
+      if (tm.rank == 0) {
+        act[L.a_off + j] = yd[j];
+        act[L.y_off + j] = yd[n + j];
+        act[L.d_off + j] = yd[2 * n + j];
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && tm.rank == 0) ctx.loss = 0.5 * np_pairwise_sum(scratch, n);
+  }
+  __syncthreads();
+  fc_bwd_rows(N, L, li, flags, job.eta_f, act, x, yd + 2 * L.cells, tm);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// conv backward (network.py:233-252).
+//   warp tasks   weight_grad of one connected pair (kernels.py:124-141): lanes
+//                split the output cells, kx*ky f64 partials, xor reduction;
+//                bias_grad of one dest map (kernels.py:144-151)
+//   thread tasks pull_bwd of one source cell (kernels.py:90-121) in the
+//                reference's order (dests k, rows y, cols x) with one f64
+//                accumulator, routed through emit_delta
+// The layer's deltas (and the source activations when they fit) are staged in
+// shared memory.  With F_UPDATE (only without F_PULL: the pull reads the old
+// weights) the weights are updated in place.
+template <int KX, int KY>
+__device__ __forceinline__ void wgrad_pair(const LayerDev& L, const LayerDev& S, int p,
+                                           const float* dl, const float* ys, float* arena,
+                                           float* g, bool upd, float eta_f) {
+  const int lane = lane_id();
+  const int hw = L.h * L.w;
+  const float* d = dl + L.pair_dst[p] * hw;
+  const float* s = ys + L.fwd_src[p] * (S.h * S.w);
+  const int o = L.fwd_widx[p];
+  if constexpr (KX > 0) {
+    constexpr int KK = KX * KY;
+    double part[KK];
+#pragma unroll
+    for (int t = 0; t < KK; ++t) part[t] = 0.0;
+    for (int cell = lane; cell < hw; cell += 32) {
+      const int r = cell / L.w, c = cell % L.w;
+      const float dv = d[cell];
+      const float* base = s + (r * L.ty) * S.w + c * L.tx;
+#pragma unroll
+      for (int t = 0; t < KK; ++t) {
+        const int v = t / KX, u = t % KX;
+        part[t] += (double)__fmul_rn(dv, base[v * S.w + u]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      const double sum = warp_sum(part[t]);
+      if (lane == t % 32) {
+        if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)sum);
+        else g[o + t] = (float)sum;
+      }
+    }
+  } else {
+    const int kk = L.kx * L.ky;
+    for (int t = 0; t < kk; ++t) {
+      const int v = t / L.kx, u = t % L.kx;
+      double part = 0.0;
+      for (int cell = lane; cell < hw; cell += 32) {
+        const int r = cell / L.w, c = cell % L.w;
+        part += (double)__fmul_rn(d[cell], s[(r * L.ty + v) * S.w + c * L.tx + u]);
+      }
+      const double sum = warp_sum(part);
+      if (lane == 0) {
+        if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)sum);
+        else g[o + t] = (float)sum;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, int flags,
+                                            float eta_f, float* act, const TeamCtx& tm) {
+  const int li = &L - N.L;
+  const LayerDev& S = N.L[li - 1];
   float* arena = N.params + L.p_off;
   float* g = N.grads + L.p_off;
   const bool upd = flags & F_UPDATE;
-  const int kk = L.kx * L.ky;
   const int hw = L.h * L.w, shw = S.h * S.w;
-  const int n_w = L.n_pairs * kk;
-  const int n_b = L.maps;
-  const int n_p = (flags & F_PULL) ? S.cells : 0;
-  const int total = n_w + n_b + n_p;
-  for (int q = gtid; q < total; q += gsize) {
-    if (q < n_w) {
-      const int p = q / kk, vu = q % kk;
-      const int v = vu / L.kx, u = vu % L.kx;
-      const float* d = dl + L.pair_dst[p] * hw;
-      const float* s = ys + L.fwd_src[p] * shw + v * S.w + u;
-      double acc = 0.0;
-      for (int r = 0; r < L.h; ++r) {
-        const float* srow = s + r * L.ty * S.w;
-        const float* drow = d + r * L.w;
-        for (int c = 0; c < L.w; ++c)
-          acc = __dadd_rn(acc, (double)__fmul_rn(drow[c], srow[c * L.tx]));
-      }
-      const int o = L.fwd_widx[p] + vu;
-      if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
-      else g[o] = (float)acc;
-    } else if (q < n_w + n_b) {
-      const int d = q - n_w;
+  const int lane = lane_id();
+  int used = 0;
+  const float* dl = stage(act + L.d_off, L.cells, tm, used);
+  const float* ys = stage(act + S.y_off, S.cells, tm, used);
+  __syncthreads();
+  const int n_w = L.n_pairs;
+  const int total = n_w + L.maps;
+  const Span ts = cta_span(total, tm);
+  for (int task = ts.b + (threadIdx.x >> 5); task < ts.e; task += blockDim.x >> 5) {
+    if (task < n_w) {
+      if (L.kx == 2 && L.ky == 2) wgrad_pair<2, 2>(L, S, task, dl, ys, arena, g, upd, eta_f);
+      else if (L.kx == 3 && L.ky == 3) wgrad_pair<3, 3>(L, S, task, dl, ys, arena, g, upd, eta_f);
+      else if (L.kx == 4 && L.ky == 4) wgrad_pair<4, 4>(L, S, task, dl, ys, arena, g, upd, eta_f);
+      else if (L.kx == 5 && L.ky == 5) wgrad_pair<5, 5>(L, S, task, dl, ys, arena, g, upd, eta_f);
+      else wgrad_pair<0, 0>(L, S, task, dl, ys, arena, g, upd, eta_f);
+    } else {
+      const int d = task - n_w;
       const float* dd = dl + d * hw;
       double acc = 0.0;
-      for (int i = 0; i < hw; ++i) acc = __dadd_rn(acc, (double)dd[i]);
-      const int o = L.bias_off[d];
-      if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
-      else g[o] = (float)acc;
-    } else {
-      const int cell = q - n_w - n_b;
+      for (int i = lane; i < hw; i += 32) acc += (double)dd[i];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const int o = L.bias_off[d];
+        if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
+        else g[o] = (float)acc;
+      }
+    }
+  }
+  if (flags & F_PULL) {
+    const Span cs = cta_span(S.cells, tm);
+    for (int cell = cs.b + threadIdx.x; cell < cs.e; cell += blockDim.x) {
       const int s = cell / shw, pix = cell % shw;
       const int j = pix / S.w, i = pix % S.w;
       const int ylo = ceil_div_clamp0(j - L.ky + 1, L.ty);
       const int yhi = min(j / L.ty, L.h - 1);
       const int xlo = ceil_div_clamp0(i - L.kx + 1, L.tx);
       const int xhi = min(i / L.tx, L.w - 1);
-      double acc = 0.0;
-      const int k1 = L.bwd_off[s + 1];
-      for (int k = L.bwd_off[s]; k < k1; ++k) {
-        const float* d = dl + L.bwd_dst[k] * hw;
-        const float* w = arena + L.bwd_widx[k];
+      // four interleaved accumulators over the destination list (fixed
+      // combination order), so the f64 adds overlap
+      // The covering window (ylo..yhi, xlo..xhi) depends only on the source
+      // cell, so four destinations share one loop nest: accumulator q takes
+      // the destinations k = kb + q (mod 4), combined in fixed order.
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      const int kb = L.bwd_off[s], k1 = L.bwd_off[s + 1];
+      const int dw0 = (j - ylo * L.ty) * L.kx + i - xlo * L.tx;   // weight index at (ylo, xlo)
+      int k = kb;
+      for (; k + 4 <= k1; k += 4) {
+        const float* d0 = dl + L.bwd_dst[k] * hw + ylo * L.w;
+        const float* d1 = dl + L.bwd_dst[k + 1] * hw + ylo * L.w;
+        const float* d2 = dl + L.bwd_dst[k + 2] * hw + ylo * L.w;
+        const float* d3 = dl + L.bwd_dst[k + 3] * hw + ylo * L.w;
+        const float* w0 = arena + L.bwd_widx[k] + dw0;
+        const float* w1 = arena + L.bwd_widx[k + 1] + dw0;
+        const float* w2 = arena + L.bwd_widx[k + 2] + dw0;
+        const float* w3 = arena + L.bwd_widx[k + 3] + dw0;
         for (int y = ylo; y <= yhi; ++y) {
-          const float* wrow = w + (j - y * L.ty) * L.kx + i;
-          const float* drow = d + y * L.w;
-          for (int x = xlo; x <= xhi; ++x)
-            acc = __dadd_rn(acc, (double)__fmul_rn(drow[x], wrow[-x * L.tx]));
+          for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx) {
+            acc[0] += (double)__fmul_rn(d0[x], w0[wi]);
+            acc[1] += (double)__fmul_rn(d1[x], w1[wi]);
+            acc[2] += (double)__fmul_rn(d2[x], w2[wi]);
+            acc[3] += (double)__fmul_rn(d3[x], w3[wi]);
+          }
+          d0 += L.w; d1 += L.w; d2 += L.w; d3 += L.w;
+          w0 -= L.ty * L.kx; w1 -= L.ty * L.kx; w2 -= L.ty * L.kx; w3 -= L.ty * L.kx;
         }
       }
-      emit_delta(N, act, li - 1, cell, (float)acc);
+      for (; k < k1; ++k) {
+        const float* d = dl + L.bwd_dst[k] * hw + ylo * L.w;
+        const float* w = arena + L.bwd_widx[k] + dw0;
+        double part = 0.0;
+        for (int y = ylo; y <= yhi; ++y, d += L.w, w -= L.ty * L.kx)
+          for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx)
+            part += (double)__fmul_rn(d[x], w[wi]);
+        switch ((k - kb) & 3) {
+          case 0: acc[0] += part; break;
+          case 1: acc[1] += part; break;
+          case 2: acc[2] += part; break;
+          default: acc[3] += part; break;
+        }
+      }
+      emit_delta(N, act, li - 1, cell, (float)((acc[0] + acc[1]) + (acc[2] + acc[3])));
     }
   }
+  __syncthreads();
 }
 
 __device__ __forceinline__ void op_update(const NetDev& N, const LayerDev& L, float eta_f,
-                                          int gtid, int gsize) {
+                                          const TeamCtx& tm) {
   float* p = N.params + L.p_off;
   const float* g = N.grads + L.p_off;
-  for (int64_t q = gtid; q < L.n_par; q += gsize) p[q] = sgd(p[q], eta_f, g[q]);
+  const Span sp = cta_span(L.n_par, tm);
+  for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) p[q] = sgd(p[q], eta_f, g[q]);
 }
 
-// Runs the ops of one phase for this thread's share of the team.
+// Runs the ops of one phase for this thread's share of the team.  Every
+// thread of every CTA calls this (ops may __syncthreads internally).
 __device__ __forceinline__ void run_phase(const NetDev& N, const Program& P, int ph,
-                                          const Job& job, Ctx& ctx, int team_rank,
-                                          int gtid, int gsize, double* scratch) {
+                                          const Job& job, Ctx& ctx, const TeamCtx& tm,
+                                          double* scratch) {
   for (int o = P.begin[ph]; o < P.begin[ph + 1]; ++o) {
     const Op op = P.ops[o];
     const LayerDev& L = N.L[op.layer];
     switch (op.kind) {
-      case OP_LOAD_INPUT: op_load_input(N, job, ctx, gtid, gsize); break;
-      case OP_IMGPROC: op_imgproc(N, L, ctx.act, gtid, gsize); break;
-      case OP_CONV_FWD: op_conv_fwd(N, L, op.flags, ctx.act, gtid, gsize); break;
-      case OP_POOL_FWD: op_pool_fwd(N, L, ctx.act, gtid, gsize); break;
-      case OP_FC_FWD: op_fc_fwd(N, L, ctx.act, gtid, gsize); break;
-      case OP_ZERO_DELTA: op_zero_delta(L, ctx.act, gtid, gsize); break;
+      case OP_LOAD_INPUT: op_load_input(N, job, ctx, tm); break;
+      case OP_IMGPROC: op_imgproc(N, L, ctx.act, tm); break;
+      case OP_CONV_FWD: op_conv_fwd(N, L, op.flags, ctx.act, tm); break;
+      case OP_POOL_FWD: op_pool_fwd(N, L, ctx.act, tm); break;
+      case OP_FC_FWD: op_fc_fwd(N, L, ctx.act, tm); break;
+      case OP_ZERO_DELTA: op_zero_delta(L, ctx.act, tm); break;
       case OP_OUT_DELTA:
-        if (team_rank == 0 && threadIdx.x < 32) op_out_delta(N, job, ctx, scratch);
+        if (tm.rank == 0 && threadIdx.x < 32) op_out_delta(N, job, ctx, scratch);
         break;
-      case OP_FC_BWD: op_fc_bwd(N, L, op.flags, job.eta_f, ctx.act, gtid, gsize); break;
-      case OP_CONV_BWD: op_conv_bwd(N, L, op.flags, job.eta_f, ctx.act, gtid, gsize); break;
-      case OP_UPDATE: op_update(N, L, job.eta_f, gtid, gsize); break;
+      case OP_FC_BWD: op_fc_bwd(N, L, op.flags, job.eta_f, ctx.act, tm); break;
+      case OP_FC_OUT: op_fc_out(N, L, op.flags, job, ctx, tm, scratch); break;
+      case OP_CONV_BWD: op_conv_bwd(N, L, op.flags, job.eta_f, ctx.act, tm); break;
+      case OP_UPDATE: op_update(N, L, job.eta_f, tm); break;
       default: break;
     }
   }

@@ -97,12 +97,23 @@ __device__ __forceinline__ void load_desc(NetDev* dst, const NetDev* src) {
 // ---------------------------------------------------------------------------
 // persistent training / single-step kernel: one team per net.
 
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr size_t kDescBytes = (sizeof(NetDev) + 15) & ~size_t(15);
+constexpr size_t kScratchBytes = kScratchDoubles * sizeof(double);
+constexpr int kTeamStageFloats = 48 * 1024;   // 192 KB staging per CTA
+constexpr int kEvalStageFloats = 12 * 1024;   // 48 KB staging per CTA
+
 template <class Team>
 __global__ void __launch_bounds__(512, 1)
 net_team_kernel(NetPtrs nets, Job job, int ctas) {
   extern __shared__ __align__(16) unsigned char smem[];
   NetDev& N = *reinterpret_cast<NetDev*>(smem);
-  double* scratch = reinterpret_cast<double*>(smem + ((sizeof(NetDev) + 15) & ~size_t(15)));
+  double* scratch = reinterpret_cast<double*>(smem + kDescBytes);
 
   unsigned rank, team, tsize;
   if constexpr (std::is_same<Team, ClusterTeam>::value) {
@@ -118,19 +129,30 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
   load_desc(&N, nets.p[team]);
 
   const Program& P = N.prog[job.prog];
-  const int gtid = rank * blockDim.x + threadIdx.x;
-  const int gsize = tsize * blockDim.x;
+  TeamCtx tm;
+  tm.rank = rank;
+  tm.size = tsize;
+  tm.gtid = rank * blockDim.x + threadIdx.x;
+  tm.gsize = tsize * blockDim.x;
+  tm.gwarp = tm.gtid >> 5;
+  tm.gwarps = tm.gsize >> 5;
+  tm.smem = reinterpret_cast<float*>(smem + kDescBytes + kScratchBytes);
+  tm.smem_floats = kTeamStageFloats;
   Ctx ctx;
   ctx.act = N.act;
   ctx.loss = 0.0;
   double total = 0.0;
+  const bool timer = job.prof && rank == 0 && threadIdx.x == 0 && team == 0;
   for (int64_t t = 0; t < job.n; ++t) {
     ctx.t = t;
     ctx.img = job.order ? (int64_t)job.order[t] : job.first + t;
     ctx.label = job.labels ? job.labels[ctx.img] : -1;
+    const bool prof_t = timer && t < job.prof_images;
+    if (prof_t) job.prof[t * (P.n_phases + 1)] = globaltimer();
     for (int ph = 0; ph < P.n_phases; ++ph) {
-      run_phase(N, P, ph, job, ctx, rank, gtid, gsize, scratch);
+      run_phase(N, P, ph, job, ctx, tm, scratch);
       Team::sync(N, ctas);
+      if (prof_t) job.prof[t * (P.n_phases + 1) + ph + 1] = globaltimer();
     }
     if (rank == 0 && threadIdx.x == 0 && job.prog != PROG_FORWARD && job.prog != PROG_APPLY) {
       total += ctx.loss;
@@ -145,12 +167,21 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
 // runs PROG_EVAL on images first+blockIdx.x, first+blockIdx.x+gridDim.x, ...
 // Same per-neuron arithmetic as training's forward, so labels are identical.
 
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(256)
 net_eval_kernel(const NetDev* net, Job job) {
   extern __shared__ __align__(16) unsigned char smem[];
   NetDev& N = *reinterpret_cast<NetDev*>(smem);
   load_desc(&N, net);
   const Program& P = N.prog[PROG_EVAL];
+  TeamCtx tm;
+  tm.rank = 0;
+  tm.size = 1;
+  tm.gtid = threadIdx.x;
+  tm.gsize = blockDim.x;
+  tm.gwarp = threadIdx.x >> 5;
+  tm.gwarps = blockDim.x >> 5;
+  tm.smem = reinterpret_cast<float*>(smem + kDescBytes);
+  tm.smem_floats = kEvalStageFloats;
   Ctx ctx;
   ctx.act = job.eval_scratch + (int64_t)blockIdx.x * N.act_size;
   const LayerDev& O = N.L[N.n_layers - 1];
@@ -158,7 +189,7 @@ net_eval_kernel(const NetDev* net, Job job) {
     ctx.t = t;
     ctx.img = job.first + t;
     for (int ph = 0; ph < P.n_phases; ++ph) {
-      run_phase(N, P, ph, job, ctx, 0, threadIdx.x, blockDim.x, nullptr);
+      run_phase(N, P, ph, job, ctx, tm, nullptr);
       __syncthreads();
     }
     const float* y = ctx.act + O.y_off;
@@ -242,12 +273,15 @@ struct ProgramBuilder {
   }
 };
 
-void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero) {
+// `skip_out`: the output layer's forward is folded into OP_FC_OUT.
+void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero,
+                   bool skip_out = false) {
   if (load) {
     b.add(OP_LOAD_INPUT, 0);
     b.phase();
   }
-  for (int k = 1; k < N.n_layers; ++k) {
+  const int last = skip_out ? N.n_layers - 1 : N.n_layers;
+  for (int k = 1; k < last; ++k) {
     const LayerDev& L = N.L[k];
     const bool scatter_target = zero && k + 1 < N.n_layers &&
                                 N.L[k + 1].kind == L_POOL && L.has_delta;
@@ -269,13 +303,11 @@ void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero) {
 // learnable layer is updated as soon as nothing later reads its old weights:
 // FC rows in place, a conv whose pull is done in the following phase.
 void build_backward(ProgramBuilder& b, const NetDev& N, bool update) {
-  b.add(OP_OUT_DELTA, N.n_layers - 1);
-  b.phase();
   std::vector<int> pending;
   int k = N.n_layers - 1;
   bool done = false;
   while (!done && k >= 1 && N.L[k].kind == L_FC) {
-    b.add(OP_FC_BWD, k, update ? F_UPDATE : 0);
+    b.add(k == N.n_layers - 1 ? OP_FC_OUT : OP_FC_BWD, k, update ? F_UPDATE : 0);
     for (int u : pending) b.add(OP_UPDATE, u);
     pending.clear();
     b.phase();
@@ -308,7 +340,7 @@ void build_backward(ProgramBuilder& b, const NetDev& N, bool update) {
 void build_programs(NetDev& N, bool* ok) {
   {
     ProgramBuilder b(N.prog[PROG_TRAIN]);
-    build_forward(b, N, true, true);
+    build_forward(b, N, true, true, true);
     build_backward(b, N, true);
     *ok = *ok && b.ok;
   }
@@ -336,9 +368,8 @@ void build_programs(NetDev& N, bool* ok) {
   }
 }
 
-size_t team_smem_bytes() {
-  return ((sizeof(NetDev) + 15) & ~size_t(15)) + kScratchDoubles * sizeof(double);
-}
+size_t team_smem_bytes() { return kDescBytes + kScratchBytes + kTeamStageFloats * sizeof(float); }
+size_t eval_smem_bytes() { return kDescBytes + kEvalStageFloats * sizeof(float); }
 
 int configure_kernels() {
   static bool done = false;
@@ -352,7 +383,7 @@ int configure_kernels() {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CK_CUDA_TRY(cudaFuncSetAttribute(net_eval_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sizeof(NetDev)));
+                                   (int)eval_smem_bytes()));
   done = true;
   return CK_OK;
 }
@@ -574,9 +605,26 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
       fwd_widx[p] = (int)D.fwd_widx[p];
       count[s]++;
     }
+    // The kernels rely on the reference's arena tiling (topology.py:82-96):
+    // per dest map, its kx*ky blocks back to back in row order, then the bias.
+    int cursor = 0;
     for (int d = 0; d < L.maps; ++d) {
       bias[d] = (int)D.bias_offset[d];
-      for (int p = fwd_off[d]; p < fwd_off[d + 1]; ++p) pair_dst[p] = d;
+      for (int p = fwd_off[d]; p < fwd_off[d + 1]; ++p) {
+        pair_dst[p] = d;
+        if (fwd_widx[p] != cursor) {
+          delete net;
+          return set_error(CK_E_CONFIG, "layer " + std::to_string(k) +
+                                            ": arena is not tiled like ConnectionTable");
+        }
+        cursor += D.kx * D.ky;
+      }
+      if (bias[d] != cursor) {
+        delete net;
+        return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": bias slot out of place");
+      }
+      cursor += 1;
+      N.L[k].max_fan_in = std::max(N.L[k].max_fan_in, fwd_off[d + 1] - fwd_off[d]);
     }
     // backward CSR = exact transpose, destinations ascending (topology.invert_table)
     bwd_off[0] = 0;
@@ -897,6 +945,69 @@ int ck_net_train_epoch(ck_net* net, const uint8_t* images, const float* lut,
   return CK_OK;
 }
 
+int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
+                         const int32_t* labels, const int32_t* order, int64_t n, double eta,
+                         int64_t* phase_ns, int max_phases, int* n_phases) {
+  CK_CHECK(net && images && labels && phase_ns && n_phases, CK_E_CONFIG, "null argument");
+  CK_CHECK(n >= 1 && eta > 0, CK_E_CONFIG, "need images and a positive learning rate");
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  const int np = net->h.prog[PROG_TRAIN].n_phases;
+  *n_phases = np;
+  CK_CHECK(max_phases >= np, CK_E_DIMENSION, "phase buffer too small");
+  long long* d_prof = nullptr;
+  CK_CUDA_TRY(cudaMalloc((void**)&d_prof, sizeof(long long) * n * (np + 1)));
+  Job job = empty_job(PROG_TRAIN);
+  job.images = images;
+  job.lut = lut;
+  job.labels = labels;
+  job.order = order;
+  job.n = n;
+  job.eta_f = (float)eta;
+  job.loss_total = net->d_loss;
+  job.prof = d_prof;
+  job.prof_images = n;
+  int rc = launch_teams(&net, 1, job, net->stream);
+  std::vector<long long> h((size_t)n * (np + 1));
+  if (rc == CK_OK) {
+    cudaError_t e = cudaMemcpyAsync(h.data(), d_prof, sizeof(long long) * h.size(),
+                                    cudaMemcpyDeviceToHost, net->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(net->stream);
+    if (e != cudaSuccess) rc = cuda_status(e, "read phase profile");
+  }
+  cudaFree(d_prof);
+  if (rc) return rc;
+  for (int p = 0; p < np; ++p) {
+    long long sum = 0;
+    for (int64_t t = 0; t < n; ++t) sum += h[t * (np + 1) + p + 1] - h[t * (np + 1) + p];
+    phase_ns[p] = sum / n;
+  }
+  return CK_OK;
+}
+
+int ck_net_describe_program(const ck_net* net, int prog, char* buf, int cap) {
+  CK_CHECK(net && buf && cap > 0, CK_E_CONFIG, "null argument");
+  CK_CHECK(prog >= 0 && prog < N_PROGS, CK_E_CONFIG, "unknown program");
+  static const char* names[] = {"load_input", "imgproc", "conv_fwd", "pool_fwd", "fc_fwd",
+                                "zero_delta", "out_delta", "fc_bwd", "conv_bwd", "update",
+                                "fc_out"};
+  const Program& P = net->h.prog[prog];
+  std::string s;
+  for (int ph = 0; ph < P.n_phases; ++ph) {
+    s += "phase " + std::to_string(ph) + ":";
+    for (int o = P.begin[ph]; o < P.begin[ph + 1]; ++o) {
+      const Op& op = P.ops[o];
+      s += std::string(" ") + names[op.kind] + "(L" + std::to_string(op.layer);
+      if (op.flags & F_UPDATE) s += ",update";
+      if (op.flags & F_PULL) s += ",pull";
+      if (op.flags & F_ZERO_SELF) s += ",zero";
+      s += ")";
+    }
+    s += "\n";
+  }
+  snprintf(buf, cap, "%s", s.c_str());
+  return CK_OK;
+}
+
 int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut, int64_t first,
                 int64_t n, int32_t* pred, float* outputs, ck_stream_t stream) {
   CK_CHECK(net && images && pred, CK_E_CONFIG, "null argument");
@@ -924,7 +1035,7 @@ int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut, int64_t fi
   job.pred = pred;
   job.outputs = outputs;
   job.eval_scratch = net->d_eval;
-  net_eval_kernel<<<ctas, 256, sizeof(NetDev), (cudaStream_t)stream>>>(net->d_desc, job);
+  net_eval_kernel<<<ctas, 256, eval_smem_bytes(), (cudaStream_t)stream>>>(net->d_desc, job);
   count_launch();
   CK_CUDA_TRY(cudaGetLastError());
   return CK_OK;

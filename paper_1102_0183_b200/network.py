@@ -79,8 +79,9 @@ class LayerView:
 
     def _arg(self):
         flat = self._read(BUF_ARG, np.int32)
-        src_w = self._net.spec.layers[self.index - 1].out_width
-        return flat // src_w, flat % src_w
+        src = self._net.spec.layers[self.index - 1]
+        local = flat % (src.out_height * src.out_width)
+        return local // src.out_width, local % src.out_width
 
     @property
     def arg_r(self) -> np.ndarray:
@@ -207,6 +208,13 @@ class NetworkState:
         k, c, t = C.c_int(), C.c_int(), C.c_int()
         _lib.call("ck_net_get_team", self.handle, C.byref(k), C.byref(c), C.byref(t))
         return k.value, c.value, t.value
+
+    def describe_program(self, prog: int = 0) -> str:
+        """Phase program of the engine (0 train, 1 forward, 2 backward,
+        3 apply, 4 eval)."""
+        buf = C.create_string_buffer(1 << 14)
+        _lib.call("ck_net_describe_program", self.handle, prog, buf, len(buf))
+        return buf.value.decode()
 
     # -- parameters ----------------------------------------------------
 

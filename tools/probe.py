@@ -65,6 +65,9 @@ def main():
             except Exception as exc:  # keep probing other shapes
                 print(f"{name} team={team} failed: {exc}", flush=True)
         net = ck.NetworkState(spec, 0)
+        print(net.describe_program(0), flush=True)
+        ph = ck.training.profile_phases(net, data.limit(200))
+        print(f"{name} phase ns:", ph.tolist(), "sum", int(ph.sum()), flush=True)
         ck.predict_batch(net, data.limit(10))
         ms = timed(lambda: ck.predict_batch(net, data))
         print(f"{name} eval: {ms:.2f} ms / {n} -> {n / ms * 1e3:.0f} img/s", flush=True)
