@@ -918,8 +918,6 @@ int ck_net_train_epoch(ck_net* net, const uint8_t* images, const float* lut,
                        const int32_t* labels, const int32_t* order, int64_t n, double eta,
                        double* losses, double* mean_loss, ck_stream_t stream) {
   CK_CHECK(net, CK_E_CONFIG, "null net");
-  if (!losses) return ck_committee_train_epoch(&net, 1, images, lut, labels, order, n, eta,
-                                               mean_loss, stream);
   CK_CHECK(images && labels, CK_E_CONFIG, "null dataset pointer");
   CK_CHECK(n >= 1, CK_E_CONFIG, "empty epoch");
   CK_CHECK(eta > 0, CK_E_CONFIG, "learning rate must be > 0");

@@ -34,6 +34,12 @@ class DeviceDataset:
         self.n = len(data)
         self.device = device
         self.in_shape = (data.channels, data.height, data.width)
+        pinned = getattr(data, "_pinned", None)
+        if pinned is not None:      # page-locked host copies: async uploads
+            self.images = pinned["images"].to(dev, non_blocking=True)
+            self.lut = pinned["lut"].to(dev, non_blocking=True)
+            self.labels = pinned["labels"].to(dev, non_blocking=True)
+            return
         if data.raw is not None:
             self.images = torch.from_numpy(np.ascontiguousarray(data.raw)).to(dev)
             self.lut = torch.from_numpy(byte_lut()).to(dev)
@@ -50,6 +56,27 @@ class DeviceDataset:
     @property
     def lut_ptr(self) -> int | None:
         return None if self.lut is None else self.lut.data_ptr()
+
+
+def pin_dataset(data: Dataset) -> Dataset:
+    """Keep page-locked host copies of ``data``'s bytes, LUT and labels so
+    that every upload (DeviceDataset) is an async copy from pinned memory."""
+    if data.raw is None:
+        raise StateError("only byte datasets (from_bytes) can be pinned")
+    torch = torch_cuda()
+    data._pinned = {
+        "images": torch.from_numpy(np.ascontiguousarray(data.raw)).pin_memory(),
+        "lut": torch.from_numpy(byte_lut()).pin_memory(),
+        "labels": torch.from_numpy(np.ascontiguousarray(data.labels, np.int32)).pin_memory(),
+    }
+    return data
+
+
+def upload_bytes(data: Dataset) -> int:
+    """Host->device bytes one DeviceDataset upload of ``data`` moves."""
+    n = data.raw.nbytes if data.raw is not None else len(data) * data.channels * \
+        data.height * data.width * 4
+    return int(n + 4 * len(data) + (1024 if data.raw is not None else 0))
 
 
 def device_dataset(data: Dataset, device: int = 0) -> DeviceDataset:
