@@ -138,7 +138,9 @@ typedef struct ck_net ck_net;
 
 /* Execution team used by the persistent training kernel:
  * CK_TEAM_CLUSTER = one thread-block cluster per net (hardware cluster
- * barrier, up to 16 CTAs); CK_TEAM_GRID = one cooperative grid per net. */
+ * barrier, up to 16 CTAs); CK_TEAM_GRID = one cooperative grid per net;
+ * CK_TEAM_AUTO (default) = a grid team of one CTA per SM, the SMs split
+ * evenly between the nets of one launch.  Results do not depend on the team. */
 enum { CK_TEAM_AUTO = 0, CK_TEAM_CLUSTER = 1, CK_TEAM_GRID = 2 };
 
 int ck_net_create(const ck_layer_desc* layers, int n_layers, int device,
@@ -194,8 +196,10 @@ int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut,
                 int64_t first, int64_t n, int32_t* pred, float* outputs,
                 ck_stream_t stream);
 
-/* Instrumented PROG_TRAIN run over n images: average device time of every
- * phase (team barrier to team barrier, %globaltimer ns) into phase_ns. */
+/* Instrumented PROG_TRAIN run over n images (%globaltimer ns, averaged):
+ * phase_ns[p] = the slowest CTA's work in phase p (previous barrier exit to
+ * its last warp done), phase_ns[n_phases + p] = the barrier after it (slowest
+ * work end to barrier exit).  max_phases must be >= 2 * n_phases. */
 int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
                          const int32_t* labels, const int32_t* order, int64_t n,
                          double eta, int64_t* phase_ns, int max_phases,

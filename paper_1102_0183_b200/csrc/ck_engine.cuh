@@ -32,6 +32,8 @@ constexpr int kMaxOps = 80;
 constexpr int kMaxPhases = 56;
 constexpr int kFcSlices = 16;      // FC forward: i-slices combined in fixed order
 constexpr int kPullLanes = 8;      // pull: lanes per source cell
+constexpr int kFcTile = 8;         // FC forward: output columns per CTA tile
+constexpr int kStageMax = 4096;    // largest per-layer array every CTA copies
 
 enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
 
@@ -45,8 +47,11 @@ struct LayerDev {
   int has_delta;
   int n_filt, fh, fw;              // imgproc
   int max_fan_in;                  // conv: largest forward row
+  int pool_above;                  // conv: the next layer is a max-pool (sparse backward)
+  int wg_winner_major;             // conv: sparse weight_grad splits winners over lanes
   int64_t p_off, b_off, n_par;     // params: conv arena / FC W, FC bias, count
   int64_t y_off, a_off, d_off, arg_off;  // act arena offsets (elements)
+  int64_t wrc_off, wd_off;         // pool over a conv: winner (r<<16|c), winner delta
   const int* fwd_off;              // conv tables (device, int32)
   const int* fwd_src;
   const int* fwd_widx;
@@ -70,6 +75,7 @@ enum OpKind {
   OP_CONV_BWD,        // weight/bias grads (+ update) and pulled delta below
   OP_UPDATE,          // params[p_off, +n_par) -= eta * grads
   OP_FC_OUT,          // output layer: forward + output deltas + loss + backward rows
+  OP_CONV_POOL,       // conv a, y fused with the max-pool above it (y, argmax)
 };
 
 enum OpFlags { F_UPDATE = 1, F_PULL = 2, F_ZERO_SELF = 4 };
@@ -123,6 +129,8 @@ struct Job {
   float* eval_scratch;     // eval: per-CTA act arenas
   long long* prof;         // phase end times (globaltimer ns), nullable
   int64_t prof_images;     // images profiled
+  int full;                // 1: also compute values nothing downstream reads (conv
+                           // cells a pool truncates, dense conv deltas) for readback
 };
 
 struct Ctx {
@@ -150,13 +158,35 @@ struct Span {
   int b, e;
 };
 __device__ __forceinline__ Span cta_span(int64_t n, const TeamCtx& tm) {
-  return Span{(int)(n * tm.rank / tm.size), (int)(n * (tm.rank + 1) / tm.size)};
+  // 32-bit unsigned arithmetic (n * size < 2^32 for every layer we accept)
+  const unsigned un = (unsigned)n, r = (unsigned)tm.rank, sz = (unsigned)tm.size;
+  return Span{(int)(un * r / sz), (int)(un * (r + 1) / sz)};
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory staging.  Copies are issued as cp.async (LDGSTS): a thread
+// never waits on one copy before issuing the next, so staging any amount is
+// one L2 round trip.  stage_sync() (= wait for this thread's copies, then
+// __syncthreads) must separate the staging from the first read.  16-byte
+// copies use .cg (L2 only); data produced by other CTAs in the previous phase
+// is then never read through a stale L1 line.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void stage_sync() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -172,9 +202,17 @@ __device__ __forceinline__ void emit_delta(const NetDev& N, float* act, int s,
     if (L.kind == L_POOL) {
       act[L.d_off + cell] = v;
       if (!N.L[s - 1].has_delta) return;
-      cell = reinterpret_cast<const int*>(act + L.arg_off)[cell];
+      const int q = cell;
+      cell = reinterpret_cast<const int*>(act + L.arg_off)[q];
       v = __fadd_rn(0.0f, v);
       --s;
+      const LayerDev& C = N.L[s];
+      if (C.kind == L_CONV) {   // the winner's delta, also kept compact per pooled cell
+        const float dv = __fmul_rn(v, act_deriv(act[C.a_off + cell]));
+        act[C.d_off + cell] = dv;
+        act[L.wd_off + q] = dv;
+        return;
+      }
       continue;
     }
     if (L.kind == L_CONV || L.kind == L_FC)
@@ -297,10 +335,10 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   const float* src_g = act + S.y_off;
   for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = L.fwd_src[k0 + k] * (S.h * S.w);
   if (w_in_smem)
-    for (int i = threadIdx.x; i < n_w; i += blockDim.x) ws[i] = arena[w0 + i];
+    for (int i = threadIdx.x; i < n_w; i += blockDim.x) cp_async4(ws + i, arena + w0 + i);
   if (s_in_smem)
-    for (int i = threadIdx.x; i < n_src; i += blockDim.x) ss[i] = src_g[i];
-  __syncthreads();
+    for (int i = threadIdx.x; i < n_src; i += blockDim.x) cp_async4(ss + i, src_g + i);
+  stage_sync();
   const float* wbase = w_in_smem ? ws : arena + w0;
   const float* sbase = s_in_smem ? ss : src_g;
   const int* offs = w_in_smem ? soff : nullptr;
@@ -364,72 +402,256 @@ __device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L, 
       }
     y[q] = best;
     arg[q] = best_i;
+    if (S.kind == L_CONV) {
+      const int local = best_i - base;
+      reinterpret_cast<int*>(act + L.wrc_off)[q] = ((local / S.w) << 16) | (local % S.w);
+    }
   }
 }
 
-// ---------------------------------------------------------------------------
-// shared-memory staging helper: copy n floats into the CTA's scratch when
-// they fit, else keep reading global memory (the caller __syncthreads()).
+// Copy n floats into the CTA's scratch when they fit (and n <= max_n), else
+// keep reading global memory.
 __device__ __forceinline__ const float* stage(const float* src, int n, const TeamCtx& tm,
-                                              int& used) {
-  if (used + n > tm.smem_floats) return src;
+                                              int& used, int max_n = 1 << 30) {
+  if (n > max_n || used + n > tm.smem_floats) return src;
   float* dst = tm.smem + used;
-  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-    const int n4 = n >> 2;
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) d4[i] = s4[i];
-    for (int i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  int head = 0;
+  if (((reinterpret_cast<uintptr_t>(src) ^ reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    head = (int)(((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) >> 2);
+    if (head > n) head = n;
+    const int n4 = (n - head) >> 2;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x)
+      cp_async16(dst + head + 4 * i, src + head + 4 * i);
+    for (int i = head + (n4 << 2) + threadIdx.x; i < n; i += blockDim.x)
+      cp_async4(dst + i, src + i);
   } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    head = n;
   }
+  for (int i = threadIdx.x; i < head; i += blockDim.x) cp_async4(dst + i, src + i);
   used += (n + 3) & ~3;
   return dst;
 }
 
 // ---------------------------------------------------------------------------
-// FC forward (network.py:193-199).  One 32-column tile: lanes own columns,
-// the n_in rows are cut into kFcSlices interleaved slices (warps), and the
-// f64 partials are combined in slice order — independent of launch shape.
-// Returns a_j (valid in warp 0 for j < n_out); all threads must call.
-__device__ __forceinline__ float fc_tile_preact(const float* x, const float* W, const float* b,
-                                                int n_in, int n_out, int tile, double* red) {
-  const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int j = tile * 32 + lane;
-  for (int sl = warp; sl < kFcSlices; sl += nwarps) {
+// conv forward fused with the max-pool above it (kernels.py:70-87 then
+// :154-172).  Work is split by POOLED cells: a CTA computes every conv cell
+// of its pool blocks (same per-cell arithmetic as conv_fwd_chunk), keeps the
+// block's y in shared memory and picks the winner there (strict '>', first
+// cell in row-major scan).  Conv cells a pool truncates feed nothing
+// downstream; they are computed only for readback (job.full).
+
+// One conv cell from global weights (used for the truncated cells).
+template <int KX, int KY>
+__device__ __forceinline__ float conv_value_global(const LayerDev& L, const LayerDev& S,
+                                                   const float* arena, const float* src,
+                                                   int d, int r, int c) {
+  const int kk = L.kx * L.ky;
+  const int kb = L.fwd_off[d], ke = L.fwd_off[d + 1];
+  const float* w = arena + L.fwd_widx[kb];
+  float acc = arena[L.bias_off[d]];
+  const int rc = (r * L.ty) * S.w + c * L.tx;
+  for (int k = kb; k < ke; ++k) {
+    const int so = L.fwd_src[k] * (S.h * S.w);
+    acc = conv_cell<KX, KY>(acc, src + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
+  }
+  return acc;
+}
+
+template <int KX, int KY>
+__device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, bool full,
+                              float* act, const TeamCtx& tm) {
+  const int li = &L - N.L;
+  const LayerDev& S = N.L[li - 1];
+  const LayerDev& P = N.L[li + 1];
+  const int hw = L.h * L.w, shw = S.h * S.w, phw = P.h * P.w, blk = P.px * P.py;
+  const int kk = L.kx * L.ky;
+  const float* arena = N.params + L.p_off;
+  float* a = act + L.a_off;
+  float* y = act + L.y_off;
+  float* dl = act + L.d_off;
+  float* pyv = act + P.y_off;
+  int* parg = reinterpret_cast<int*>(act + P.arg_off);
+  int* pwrc = reinterpret_cast<int*>(act + P.wrc_off);
+  const Span sp = cta_span(P.cells, tm);
+  int used = 0;
+  const float* src_g = act + S.y_off;
+  const float* src = src_g;
+  if (sp.b < sp.e && S.cells <= tm.smem_floats / 2) {
+    // the whole source layer, unless this CTA's maps connect to fewer cells
+    const int nk_all = L.fwd_off[(sp.e - 1) / phw + 1] - L.fwd_off[sp.b / phw];
+    if (S.cells <= nk_all * shw) src = stage(src, S.cells, tm, used);
+  }
+  const bool whole = src != src_g;
+  const bool zero = full && (flags & F_ZERO_SELF);
+  // The arena is tiled like ConnectionTable (checked at ck_net_create): dest
+  // map d's blocks start at fwd_off[d]*kk + d and its bias sits at
+  // fwd_off[d+1]*kk + d, so the chunk plan needs fwd_off alone.
+  for (int q = sp.b; q < sp.e;) {
+    // chunk [q, qe): block outputs (+ its weights and source offsets when they fit)
+    // (with the source layer not staged whole, a copy of each connected
+    // source map too -- sparse tables need far less than the whole layer)
+    const int avail = tm.smem_floats - used;
+    int qe = min(sp.e, q + avail / blk);
+    bool wst = false, slots = false;
+    for (int tries = 0; tries < 24; ++tries) {
+      const int d0 = q / phw, d1 = (qe - 1) / phw;
+      const int nk = L.fwd_off[d1 + 1] - L.fwd_off[d0];
+      const int nw = nk * kk + d1 + 1 - d0;
+      const int base = ((nk + 3) & ~3) + ((nw + 3) & ~3) + (qe - q) * blk;
+      if (!whole && base + nk * shw <= avail) { wst = slots = true; break; }
+      if (whole && base <= avail) { wst = true; break; }
+      if (qe - q <= phw) {
+        wst = base <= avail;
+        break;
+      }
+      qe = q + max(phw, (qe - q) / 2);
+    }
+    const int d0 = q / phw, d1 = (qe - 1) / phw;
+    const int k0 = L.fwd_off[d0], k1 = L.fwd_off[d1 + 1];
+    const int w0 = k0 * kk + d0;
+    const int nw = (k1 - k0) * kk + d1 + 1 - d0;
+    int* soff = reinterpret_cast<int*>(tm.smem + used);
+    float* ws = tm.smem + used + ((k1 - k0 + 3) & ~3);
+    float* ybuf = wst ? ws + ((nw + 3) & ~3) : tm.smem + used;
+    float* sslot = ybuf + (qe - q) * blk;
+    const float* sbase = slots ? sslot : src;
+    if (wst) {
+      int u2 = used + ((k1 - k0 + 3) & ~3);
+      stage(arena + w0, nw, tm, u2);
+      for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x)
+        soff[k] = slots ? k * shw : L.fwd_src[k0 + k] * shw;
+      if (slots)
+        for (int e = threadIdx.x; e < (k1 - k0) * shw; e += blockDim.x)
+          cp_async4(sslot + e, src_g + L.fwd_src[k0 + e / shw] * shw + e % shw);
+    }
+    stage_sync();
+    const int n_items = (qe - q) * blk;
+    for (int it = threadIdx.x; it < n_items; it += blockDim.x) {
+      const int qq = q + it / blk, t = it % blk;
+      const int d = qq / phw, pp = qq % phw;
+      const int r = (pp / P.w) * P.py + t / P.px;
+      const int c = (pp % P.w) * P.px + t % P.px;
+      float acc;
+      if (wst) {
+        const int kb = L.fwd_off[d], ke = L.fwd_off[d + 1];
+        const float* w = ws + (kb * kk + d - w0);
+        acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
+                                soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+      } else {
+        acc = conv_value_global<KX, KY>(L, S, arena, src, d, r, c);
+      }
+      const int cell = d * hw + r * L.w + c;
+      const float yv = conv_act(acc);
+      a[cell] = acc;
+      y[cell] = yv;
+      ybuf[it] = yv;
+      if (zero) dl[cell] = 0.0f;
+    }
+    __syncthreads();
+    for (int qi = threadIdx.x; qi < qe - q; qi += blockDim.x) {
+      const float* yb = ybuf + qi * blk;
+      int bt = 0;
+      float best = yb[0];
+      for (int t = 1; t < blk; ++t)
+        if (yb[t] > best) { best = yb[t]; bt = t; }
+      const int qq = q + qi;
+      const int d = qq / phw, pp = qq % phw;
+      const int r = (pp / P.w) * P.py + bt / P.px;
+      const int c = (pp % P.w) * P.px + bt % P.px;
+      pyv[qq] = best;
+      parg[qq] = d * hw + r * L.w + c;
+      pwrc[qq] = (r << 16) | c;
+    }
+    __syncthreads();
+    q = qe;
+  }
+  if (full) {   // cells outside every pool block (rows / columns the pool drops)
+    const int rh = P.h * P.py, cw = P.w * P.px;
+    const int strip = rh * (L.w - cw);
+    const int nd = hw - rh * cw;
+    if (nd > 0) {
+      const Span ds = cta_span((int64_t)nd * L.maps, tm);
+      for (int e = ds.b + threadIdx.x; e < ds.e; e += blockDim.x) {
+        const int d = e / nd, k = e % nd;
+        int r, c;
+        if (k < strip) { r = k / (L.w - cw); c = cw + k % (L.w - cw); }
+        else { r = rh + (k - strip) / L.w; c = (k - strip) % L.w; }
+        const float acc = conv_value_global<KX, KY>(L, S, arena, act + S.y_off, d, r, c);
+        const int cell = d * hw + r * L.w + c;
+        a[cell] = acc;
+        y[cell] = conv_act(acc);
+        if (zero) dl[cell] = 0.0f;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void op_conv_pool(const NetDev& N, const LayerDev& L, int flags,
+                                             bool full, float* act, const TeamCtx& tm) {
+  if (L.kx == 2 && L.ky == 2) conv_pool_fwd<2, 2>(N, L, flags, full, act, tm);
+  else if (L.kx == 3 && L.ky == 3) conv_pool_fwd<3, 3>(N, L, flags, full, act, tm);
+  else if (L.kx == 4 && L.ky == 4) conv_pool_fwd<4, 4>(N, L, flags, full, act, tm);
+  else if (L.kx == 5 && L.ky == 5) conv_pool_fwd<5, 5>(N, L, flags, full, act, tm);
+  else conv_pool_fwd<0, 0>(N, L, flags, full, act, tm);
+}
+
+// ---------------------------------------------------------------------------
+// FC forward (network.py:193-199).  Column j's pre-activation is always
+//   f32( sum_{sl=0..15} [ f64 fma-chain over rows i = sl, sl+16, ... ] ) + b_j
+// (16 fixed interleaved slices combined in slice order), whatever the tile
+// width or team shape, so training and evaluation agree bit for bit.
+// fc_cols_preact computes ncols (<= 32) columns whose weights sit at
+// W[i * ldw + j] (global or staged); a[j] lands in out_a (shared memory).
+// All threads must call.
+__device__ __forceinline__ void fc_cols_preact(const float* x, const float* W, int ldw,
+                                               const float* b, int n_in, int ncols,
+                                               double* red, float* out_a) {
+  for (int item = threadIdx.x; item < kFcSlices * ncols; item += blockDim.x) {
+    const int col = item % ncols, sl = item / ncols;
     double part = 0.0;
-    if (j < n_out)
-      for (int i = sl; i < n_in; i += kFcSlices)
-        part = fma((double)x[i], (double)W[(int64_t)i * n_out + j], part);
-    red[sl * 32 + lane] = part;
+#pragma unroll 4
+    for (int i = sl; i < n_in; i += kFcSlices)
+      part = fma((double)x[i], (double)W[i * ldw + col], part);
+    red[sl * ncols + col] = part;
   }
   __syncthreads();
-  float aj = 0.0f;
-  if (warp == 0 && j < n_out) {
+  if (threadIdx.x < ncols) {
     double acc = 0.0;
-    for (int sl = 0; sl < kFcSlices; ++sl) acc += red[sl * 32 + lane];
-    aj = __fadd_rn((float)acc, b[j]);
+    for (int sl = 0; sl < kFcSlices; ++sl) acc += red[sl * ncols + threadIdx.x];
+    out_a[threadIdx.x] = __fadd_rn((float)acc, b[threadIdx.x]);
   }
   __syncthreads();
-  return aj;
 }
 
 __device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, float* act,
                                           const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
-  const int n_tiles = (L.cells + 31) / 32;
+  const int n_in = S.cells, n_out = L.cells;
+  const int n_tiles = (n_out + kFcTile - 1) / kFcTile;
   if (tm.rank >= n_tiles) return;
   int used = 0;
-  const float* x = stage(act + S.y_off, S.cells, tm, used);
-  double* red = reinterpret_cast<double*>(tm.smem + used);   // [kFcSlices][32]
-  __syncthreads();
+  const float* x = stage(act + S.y_off, n_in, tm, used);
+  double* red = reinterpret_cast<double*>(tm.smem + used);   // [kFcSlices][kFcTile]
+  used += 2 * kFcSlices * kFcTile;
+  float* out_a = tm.smem + used;
+  used += kFcTile;
+  const float* W = N.params + L.p_off;
+  const bool wst = used + n_in * kFcTile <= tm.smem_floats;
+  float* wt = tm.smem + used;
   for (int tile = tm.rank; tile < n_tiles; tile += tm.size) {
-    const float aj = fc_tile_preact(x, N.params + L.p_off, N.params + L.b_off, S.cells, L.cells,
-                                    tile, red);
-    const int j = tile * 32 + lane_id();
-    if ((threadIdx.x >> 5) == 0 && j < L.cells) {
-      act[L.a_off + j] = aj;
-      act[L.y_off + j] = fc_act(aj);
+    const int j0 = tile * kFcTile;
+    const int nc = min(kFcTile, n_out - j0);
+    if (wst)
+      for (int e = threadIdx.x; e < n_in * nc; e += blockDim.x)
+        cp_async4(wt + (e / nc) * nc + e % nc, W + (int64_t)(e / nc) * n_out + j0 + e % nc);
+    stage_sync();
+    fc_cols_preact(x, wst ? wt : W + j0, wst ? nc : n_out, N.params + L.b_off + j0, n_in, nc,
+                   red, out_a);
+    if (threadIdx.x < nc) {
+      const float aj = out_a[threadIdx.x];
+      act[L.a_off + j0 + threadIdx.x] = aj;
+      act[L.y_off + j0 + threadIdx.x] = fc_act(aj);
     }
   }
   __syncthreads();
@@ -437,8 +659,13 @@ __device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, fl
 
 __device__ __forceinline__ void op_zero_delta(const LayerDev& L, float* act, const TeamCtx& tm) {
   float* d = act + L.d_off;
+  // a pool over a conv also keeps compact winner deltas (wrc_off > 0 marks it)
+  float* wd = L.wrc_off > 0 ? act + L.wd_off : nullptr;
   const Span sp = cta_span(L.cells, tm);
-  for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) d[q] = 0.0f;
+  for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) {
+    d[q] = 0.0f;
+    if (wd) wd[q] = 0.0f;
+  }
 }
 
 // Output deltas (backprop.py:22-32) and the sample loss (backprop.py:35-39):
@@ -512,20 +739,16 @@ __device__ __forceinline__ void op_fc_out(const NetDev& N, const LayerDev& L, in
   float* act = ctx.act;
   int used = 0;
   const float* x = stage(act + S.y_off, S.cells, tm, used);
+  const float* W = stage(N.params + L.p_off, S.cells * L.cells, tm, used, 1 << 14);
   float* yd = tm.smem + used;                    // [a | y | delta] x n_out
   used += (3 * L.cells + 3) & ~3;
   double* red = reinterpret_cast<double*>(tm.smem + used);
-  __syncthreads();
-  const int n_tiles = (L.cells + 31) / 32;
-  for (int tile = 0; tile < n_tiles; ++tile) {
-    const float aj = fc_tile_preact(x, N.params + L.p_off, N.params + L.b_off, S.cells, L.cells,
-                                    tile, red);
-    const int j = tile * 32 + lane_id();
-    if ((threadIdx.x >> 5) == 0 && j < L.cells) {
-      yd[j] = aj;
-      yd[L.cells + j] = fc_act(aj);
-    }
+  stage_sync();
+  for (int j0 = 0; j0 < L.cells; j0 += 32) {
+    const int nc = min(32, L.cells - j0);
+    fc_cols_preact(x, W + j0, L.cells, N.params + L.b_off + j0, S.cells, nc, red, yd + j0);
   }
+  for (int j = threadIdx.x; j < L.cells; j += blockDim.x) yd[L.cells + j] = fc_act(yd[j]);
   __syncthreads();
   if (threadIdx.x < 32) {
     const int n = L.cells, lane = lane_id();
@@ -609,9 +832,258 @@ __device__ __forceinline__ void wgrad_pair(const LayerDev& L, const LayerDev& S,
   }
 }
 
+// Pool-sparse conv backward.  When a max-pool sits on top of the conv layer,
+// its deltas are zero everywhere except at the pool winners (network.py:256-
+// 261: zeroed buffer, one '+=' per pooled cell), and a zero delta adds an
+// exact +0 to the reference's f64 sums.  So weight_grad, bias_grad and
+// pull_bwd visit only the winners, read from the compact per-pooled-cell
+// arrays the forward pass (winner row/col) and emit_delta (winner delta)
+// fill.  Same products, same f64 accumulation; terms that are exactly zero
+// are skipped.
+//   weight_grad  one warp per pair: lane = (tap, group); a group walks every
+//                G-th winner of the dest map; groups combined in order
+//   bias_grad    one warp per dest map
+//   pull_bwd     one thread per source cell: for every dest map in its
+//                backward list, the pool blocks that meet the covering window,
+//                each contributing its winner when the winner lies inside
+// Tap-major: lane = (tap, group); a group walks every G-th winner of the
+// dest map; the groups are combined in group order.
+//   wr / wdd  winner (r<<16|c) and winner delta of the pair's dest map
+//   s         the pair's source map (y of the layer below)
+__device__ __forceinline__ void wgrad_pair_sparse(const LayerDev& L, const LayerDev& S,
+                                                  const LayerDev& P, int o, const int* wr,
+                                                  const float* wdd, const float* s,
+                                                  float* arena, float* g, bool upd,
+                                                  float eta_f) {
+  const int lane = lane_id();
+  const int kk = L.kx * L.ky;
+  const int phw = P.h * P.w;
+  const int G = kk >= 32 ? 1 : min(32 / kk, phw);
+  for (int t0 = 0; t0 < kk; t0 += 32) {
+    const int t = kk >= 32 ? t0 + lane : lane % kk;
+    const int grp = kk >= 32 ? 0 : lane / kk;
+    double part = 0.0;
+    if (t < kk && grp < G) {
+      const int v = t / L.kx, u = t % L.kx;
+      const float* sv = s + v * S.w + u;
+      for (int wq = grp; wq < phw; wq += G) {
+        const int rc = wr[wq];
+        part += (double)__fmul_rn(wdd[wq], sv[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx]);
+      }
+    }
+    double tot = part;
+    for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, part, (lane + gg * kk) & 31);
+    if (grp == 0 && t < kk) {
+      if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)tot);
+      else g[o + t] = (float)tot;
+    }
+  }
+}
+
+// Winner-major variant for maps with many winners: lanes split the winners,
+// each lane keeps kx*ky f64 partials, then one fixed xor tree per tap.
+template <int KX, int KY>
+__device__ __forceinline__ void wgrad_pair_winners(const LayerDev& L, const LayerDev& S,
+                                                   const LayerDev& P, int o, const int* wr,
+                                                   const float* wdd, const float* s,
+                                                   float* arena, float* g, bool upd,
+                                                   float eta_f) {
+  constexpr int KK = KX * KY;
+  const int lane = lane_id();
+  const int phw = P.h * P.w;
+  double part[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) part[t] = 0.0;
+  for (int wq = lane; wq < phw; wq += 32) {
+    const int rc = wr[wq];
+    const float dv = wdd[wq];
+    const float* base = s + (rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx;
+#pragma unroll
+    for (int t = 0; t < KK; ++t) part[t] += (double)__fmul_rn(dv, base[(t / KX) * S.w + t % KX]);
+  }
+#pragma unroll
+  for (int t = 0; t < KK; ++t) {
+    const double sum = warp_sum(part[t]);
+    if (lane == t % 32) {
+      if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)sum);
+      else g[o + t] = (float)sum;
+    }
+  }
+}
+
+__device__ __forceinline__ void wgrad_sparse(const LayerDev& L, const LayerDev& S,
+                                             const LayerDev& P, int o, const int* wr,
+                                             const float* wdd, const float* s, float* arena,
+                                             float* g, bool upd, float eta_f) {
+  if (L.wg_winner_major) {
+    if (L.kx == 2 && L.ky == 2) return wgrad_pair_winners<2, 2>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+    if (L.kx == 3 && L.ky == 3) return wgrad_pair_winners<3, 3>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+    if (L.kx == 4 && L.ky == 4) return wgrad_pair_winners<4, 4>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+    if (L.kx == 5 && L.ky == 5) return wgrad_pair_winners<5, 5>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+  }
+  wgrad_pair_sparse(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+}
+
+// Each CTA stages exactly what its share needs (one cp.async round trip per
+// chunk), then computes from shared memory:
+//   weight_grad  its pairs [p0, p1): the winners of their dest maps and one
+//                copy of each pair's source map, in chunks that fit
+//   pull_bwd     its source cells: per backward-list entry (dest d, weight
+//                block) the old kernel and d's winners, in chunks of whole
+//                source maps
+// Anything that does not fit is read in place from global memory.
+__device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, float eta_f,
+                                float* act, const TeamCtx& tm) {
+  const int li = &L - N.L;
+  const LayerDev& S = N.L[li - 1];
+  const LayerDev& P = N.L[li + 1];
+  float* arena = N.params + L.p_off;
+  float* g = N.grads + L.p_off;
+  const bool upd = flags & F_UPDATE;
+  const int shw = S.h * S.w, phw = P.h * P.w;
+  const int kk = L.kx * L.ky;
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int* wrc_g = reinterpret_cast<const int*>(act + P.wrc_off);
+  const float* wd_g = act + P.wd_off;
+  const float* ys_g = act + S.y_off;
+  const int cap = tm.smem_floats - 16;
+
+  // ---- weight gradients
+  const int n_w = L.n_pairs;
+  const Span ts = cta_span(n_w + L.maps, tm);
+  const int p1 = min(ts.e, n_w);
+  for (int c0 = ts.b; c0 < p1;) {
+    int c1 = p1, da, db, need;
+    for (;;) {
+      da = L.pair_dst[c0];
+      db = L.pair_dst[c1 - 1];
+      need = 2 * (db - da + 1) * phw + (c1 - c0) * shw + 8;
+      if (need <= cap || c1 - c0 == 1) break;
+      c1 = c0 + (c1 - c0) / 2;
+    }
+    const bool fits = need <= cap;
+    int used = 0;
+    const int* wr = wrc_g + da * phw;
+    const float* wdd = wd_g + da * phw;
+    float* slots = nullptr;
+    if (fits) {
+      wr = reinterpret_cast<const int*>(
+          stage(reinterpret_cast<const float*>(wr), (db - da + 1) * phw, tm, used));
+      wdd = stage(wdd, (db - da + 1) * phw, tm, used);
+      slots = tm.smem + used;
+      for (int e = threadIdx.x; e < (c1 - c0) * shw; e += blockDim.x) {
+        const int p = c0 + e / shw;
+        cp_async4(slots + e, ys_g + L.fwd_src[p] * shw + e % shw);
+      }
+    }
+    stage_sync();
+    for (int p = c0 + warp; p < c1; p += nwarps) {
+      const int off = (L.pair_dst[p] - da) * phw;
+      const float* sp = fits ? slots + (p - c0) * shw : ys_g + L.fwd_src[p] * shw;
+      wgrad_sparse(L, S, P, L.fwd_widx[p], wr + off, wdd + off, sp, arena, g, upd, eta_f);
+    }
+    __syncthreads();
+    c0 = c1;
+  }
+  // ---- bias gradients: one warp per dest map
+  for (int task = max(ts.b, n_w) + warp; task < ts.e; task += nwarps) {
+    const int d = task - n_w;
+    double acc = 0.0;
+    for (int wq = lane; wq < phw; wq += 32) acc += (double)wd_g[d * phw + wq];
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const int o = L.bias_off[d];
+      if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
+      else g[o] = (float)acc;
+    }
+  }
+  if (!(flags & F_PULL)) {
+    __syncthreads();
+    return;
+  }
+
+  // ---- pull: kPullLanes lanes per source cell; lane l walks the backward
+  // list entries l, l + kPullLanes, ...; partials combined by a fixed xor tree
+  const Span cs = cta_span(S.cells, tm);
+  const int grp = threadIdx.x / kPullLanes, sub = threadIdx.x % kPullLanes;
+  const unsigned gmask = ((1u << kPullLanes) - 1) << (lane & ~(kPullLanes - 1));
+  const int per_k = kk + 2 * phw;
+  for (int cell0 = cs.b; cell0 < cs.e;) {
+    const int sa = cell0 / shw;
+    int sb = (cs.e - 1) / shw;
+    int ka = L.bwd_off[sa], kb = L.bwd_off[sb + 1];
+    while ((kb - ka) * per_k > cap && sb > sa) {
+      sb = sa + (sb - sa + 1) / 2 - 1;
+      kb = L.bwd_off[sb + 1];
+    }
+    const int cell1 = min(cs.e, (sb + 1) * shw);
+    const bool fits = (kb - ka) * per_k <= cap;
+    float* wst = tm.smem;
+    int* wrs = reinterpret_cast<int*>(tm.smem + (kb - ka) * kk);
+    float* wds = tm.smem + (kb - ka) * (kk + phw);
+    if (fits) {
+      for (int e = threadIdx.x; e < (kb - ka) * kk; e += blockDim.x)
+        cp_async4(wst + e, arena + L.bwd_widx[ka + e / kk] + e % kk);
+      for (int e = threadIdx.x; e < (kb - ka) * phw; e += blockDim.x) {
+        const int src = L.bwd_dst[ka + e / phw] * phw + e % phw;
+        cp_async4(wrs + e, wrc_g + src);
+        cp_async4(wds + e, wd_g + src);
+      }
+    }
+    stage_sync();
+    for (int cell = cell0 + grp; cell < cell1; cell += blockDim.x / kPullLanes) {
+      const int sm = cell / shw, pix = cell % shw;
+      const int j = pix / S.w, i = pix % S.w;
+      const int ylo = ceil_div_clamp0(j - L.ky + 1, L.ty);
+      const int yhi = min(j / L.ty, L.h - 1);
+      const int xlo = ceil_div_clamp0(i - L.kx + 1, L.tx);
+      const int xhi = min(i / L.tx, L.w - 1);
+      double acc = 0.0;
+      if (ylo <= yhi && xlo <= xhi) {
+        const int prlo = ylo / P.py, prhi = min(yhi / P.py, P.h - 1);
+        const int pclo = xlo / P.px, pchi = min(xhi / P.px, P.w - 1);
+        const int k1 = L.bwd_off[sm + 1];
+        for (int k = L.bwd_off[sm] + sub; k < k1; k += kPullLanes) {
+          const float* wk;
+          const int* wr;
+          const float* wdd;
+          if (fits) {
+            wk = wst + (k - ka) * kk;
+            wr = wrs + (k - ka) * phw;
+            wdd = wds + (k - ka) * phw;
+          } else {
+            const int d = L.bwd_dst[k];
+            wk = arena + L.bwd_widx[k];
+            wr = wrc_g + d * phw;
+            wdd = wd_g + d * phw;
+          }
+          for (int pr = prlo; pr <= prhi; ++pr)
+            for (int pc = pclo; pc <= pchi; ++pc) {
+              const int q = pr * P.w + pc;
+              const int rc = wr[q];
+              const int r = rc >> 16, c = rc & 0xffff;
+              if (r >= ylo && r <= yhi && c >= xlo && c <= xhi)
+                acc += (double)__fmul_rn(wdd[q], wk[(j - r * L.ty) * L.kx + (i - c * L.tx)]);
+            }
+        }
+      }
+#pragma unroll
+      for (int o = kPullLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
+      if (sub == 0) emit_delta(N, act, li - 1, cell, (float)acc);
+    }
+    __syncthreads();
+    cell0 = cell1;
+  }
+}
+
 __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, int flags,
                                             float eta_f, float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
+  if (L.pool_above) {
+    conv_bwd_sparse(N, L, flags, eta_f, act, tm);
+    return;
+  }
   const LayerDev& S = N.L[li - 1];
   float* arena = N.params + L.p_off;
   float* g = N.grads + L.p_off;
@@ -621,7 +1093,7 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
   int used = 0;
   const float* dl = stage(act + L.d_off, L.cells, tm, used);
   const float* ys = stage(act + S.y_off, S.cells, tm, used);
-  __syncthreads();
+  stage_sync();
   const int n_w = L.n_pairs;
   const int total = n_w + L.maps;
   const Span ts = cta_span(total, tm);
@@ -723,6 +1195,7 @@ __device__ __forceinline__ void run_phase(const NetDev& N, const Program& P, int
       case OP_LOAD_INPUT: op_load_input(N, job, ctx, tm); break;
       case OP_IMGPROC: op_imgproc(N, L, ctx.act, tm); break;
       case OP_CONV_FWD: op_conv_fwd(N, L, op.flags, ctx.act, tm); break;
+      case OP_CONV_POOL: op_conv_pool(N, L, op.flags, job.full != 0, ctx.act, tm); break;
       case OP_POOL_FWD: op_pool_fwd(N, L, ctx.act, tm); break;
       case OP_FC_FWD: op_fc_fwd(N, L, ctx.act, tm); break;
       case OP_ZERO_DELTA: op_zero_delta(L, ctx.act, tm); break;

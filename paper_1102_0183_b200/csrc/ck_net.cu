@@ -55,31 +55,27 @@ struct ClusterTeam {
     asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
     return r;
   }
-  __device__ static void sync(const NetDev&, int) {
+  __device__ static void sync(const NetDev&, int, unsigned&) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 };
 
+// Grid team barrier: a monotonic arrival counter (zeroed before each launch).
+// Each CTA's thread 0 adds 1 with release semantics (cumulative over the
+// CTA's writes, ordered before it by bar.sync) and polls with acquire until
+// every CTA of this barrier generation has arrived.  No reset, no return
+// value on the arrival, no full fences.
 struct GridTeam {
   __device__ static unsigned rank(int ctas) { return blockIdx.x % ctas; }
   __device__ static unsigned index(int ctas) { return blockIdx.x / ctas; }
-  __device__ static void sync(const NetDev& N, int ctas) {
+  __device__ static void sync(const NetDev& N, int ctas, unsigned& target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned* count = N.bar;
-      unsigned* gen = N.bar + 1;
-      const unsigned g = ld_acquire(gen);
-      __threadfence();
-      if (atomicAdd(count, 1u) == (unsigned)ctas - 1) {
-        atomicExch(count, 0u);
-        __threadfence();
-        st_release(gen, g + 1);
-      } else {
-        while (ld_acquire(gen) == g) {
-        }
+      target += (unsigned)ctas;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(N.bar) : "memory");
+      while ((int)(ld_acquire(N.bar) - target) < 0) {
       }
-      __threadfence();
     }
     __syncthreads();
   }
@@ -142,17 +138,25 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
   ctx.act = N.act;
   ctx.loss = 0.0;
   double total = 0.0;
-  const bool timer = job.prof && rank == 0 && threadIdx.x == 0 && team == 0;
+  // profile record per image: [start, then per phase: barrier exit (rank 0),
+  // work end of every CTA (after its last warp)] -- globaltimer ns
+  const int prof_stride = 1 + P.n_phases * (1 + (int)tsize);
+  unsigned bar_target = 0;
   for (int64_t t = 0; t < job.n; ++t) {
     ctx.t = t;
     ctx.img = job.order ? (int64_t)job.order[t] : job.first + t;
     ctx.label = job.labels ? job.labels[ctx.img] : -1;
-    const bool prof_t = timer && t < job.prof_images;
-    if (prof_t) job.prof[t * (P.n_phases + 1)] = globaltimer();
+    long long* prof = (job.prof && team == 0 && t < job.prof_images)
+                          ? job.prof + t * prof_stride : nullptr;
+    if (prof && rank == 0 && threadIdx.x == 0) prof[0] = globaltimer();
     for (int ph = 0; ph < P.n_phases; ++ph) {
       run_phase(N, P, ph, job, ctx, tm, scratch);
-      Team::sync(N, ctas);
-      if (prof_t) job.prof[t * (P.n_phases + 1) + ph + 1] = globaltimer();
+      if (prof) {
+        __syncthreads();
+        if (threadIdx.x == 0) prof[1 + ph * (1 + tsize) + 1 + rank] = globaltimer();
+      }
+      Team::sync(N, ctas, bar_target);
+      if (prof && rank == 0 && threadIdx.x == 0) prof[1 + ph * (1 + tsize)] = globaltimer();
     }
     if (rank == 0 && threadIdx.x == 0 && job.prog != PROG_FORWARD && job.prog != PROG_APPLY) {
       total += ctx.loss;
@@ -231,8 +235,8 @@ struct ck_net {
   float* d_eval = nullptr;        // eval scratch arenas
   int eval_ctas = 0;
   int64_t n_params = 0;
-  int team_kind = CK_TEAM_CLUSTER;
-  int team_ctas = 16;
+  int team_kind = CK_TEAM_AUTO;   // resolved per launch (resolve_team)
+  int team_ctas = 0;
   int threads = 512;
   cudaStream_t stream = nullptr;  // private stream for the synchronous calls
   std::vector<int64_t> grad_count;  // per layer (params it owns)
@@ -285,6 +289,15 @@ void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero,
     const LayerDev& L = N.L[k];
     const bool scatter_target = zero && k + 1 < N.n_layers &&
                                 N.L[k + 1].kind == L_POOL && L.has_delta;
+    if (L.kind == L_CONV && k + 1 < last && N.L[k + 1].kind == L_POOL) {
+      // conv + the max-pool above it in one phase
+      b.add(OP_CONV_POOL, k, scatter_target ? F_ZERO_SELF : 0);
+      const bool pool_target = zero && k + 2 < N.n_layers && N.L[k + 2].kind == L_POOL;
+      if (pool_target) b.add(OP_ZERO_DELTA, k + 1);
+      b.phase();
+      ++k;
+      continue;
+    }
     switch (L.kind) {
       case L_IMGPROC: b.add(OP_IMGPROC, k); break;
       case L_CONV: b.add(OP_CONV_FWD, k, scatter_target ? F_ZERO_SELF : 0); break;
@@ -307,9 +320,13 @@ void build_backward(ProgramBuilder& b, const NetDev& N, bool update) {
   int k = N.n_layers - 1;
   bool done = false;
   while (!done && k >= 1 && N.L[k].kind == L_FC) {
-    b.add(k == N.n_layers - 1 ? OP_FC_OUT : OP_FC_BWD, k, update ? F_UPDATE : 0);
+    // every CTA reads the whole output layer in OP_FC_OUT, so its update
+    // waits for the next phase
+    const bool out = k == N.n_layers - 1;
+    b.add(out ? OP_FC_OUT : OP_FC_BWD, k, (update && !out) ? F_UPDATE : 0);
     for (int u : pending) b.add(OP_UPDATE, u);
     pending.clear();
+    if (update && out) pending.push_back(k);
     b.phase();
     --k;
     if (!N.L[k].has_delta) done = true;
@@ -388,31 +405,51 @@ int configure_kernels() {
   return CK_OK;
 }
 
+// The team a launch of n_nets nets uses.  AUTO = a cooperative grid team
+// spanning the whole GPU: one 512-thread CTA per SM, the SMs shared evenly
+// between the nets of a committee (measured faster than 16-CTA clusters on
+// every BASELINE configuration: more SMs for the wide phases, and a ~1.1 us
+// arrival-counter barrier).
+struct TeamShape {
+  int kind, ctas, threads;
+};
+
+TeamShape resolve_team(const ck_net* net, int n_nets) {
+  if (net->team_kind != CK_TEAM_AUTO) return {net->team_kind, net->team_ctas, net->threads};
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device);
+  return {CK_TEAM_GRID, std::max(1, sms / std::max(1, n_nets)), 512};
+}
+
 int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
   int rc = configure_kernels();
   if (rc) return rc;
-  const ck_net* n0 = nets[0];
+  const TeamShape t0 = resolve_team(nets[0], n_nets);
   NetPtrs ptrs;
   memset(&ptrs, 0, sizeof(ptrs));
   for (int i = 0; i < n_nets; ++i) {
-    if (nets[i]->team_kind != n0->team_kind || nets[i]->team_ctas != n0->team_ctas ||
-        nets[i]->threads != n0->threads)
+    const TeamShape ti = resolve_team(nets[i], n_nets);
+    if (ti.kind != t0.kind || ti.ctas != t0.ctas || ti.threads != t0.threads)
       return set_error(CK_E_CONFIG, "all nets of one launch need the same team config");
     ptrs.p[i] = nets[i]->d_desc;
   }
   job.n_nets = n_nets;
-  const int ctas = n0->team_ctas;
+  const int ctas = t0.ctas;
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(ctas * n_nets);
-  cfg.blockDim = dim3(n0->threads);
+  cfg.blockDim = dim3(t0.threads);
   cfg.dynamicSmemBytes = team_smem_bytes();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
-  if (n0->team_kind == CK_TEAM_GRID) {
+  if (t0.kind == CK_TEAM_GRID) {
+    for (int i = 0; i < n_nets; ++i) {   // arrival counters start at 0 every launch
+      e = cudaMemsetAsync(nets[i]->d_bar, 0, 2 * sizeof(unsigned), st);
+      if (e != cudaSuccess) return cuda_status(e, "reset grid barrier");
+    }
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     e = cudaLaunchKernelEx(&cfg, net_team_kernel<GridTeam>, ptrs, job, ctas);
@@ -439,6 +476,7 @@ Job empty_job(int prog) {
 int run_single(ck_net* net, Job job) {
   CK_CUDA_TRY(cudaSetDevice(net->device));
   job.loss_total = net->d_loss;
+  job.full = 1;   // per-sample API: every buffer is readable afterwards
   int rc = launch_teams(&net, 1, job, net->stream);
   if (rc) return rc;
   CK_CUDA_TRY(cudaStreamSynchronize(net->stream));
@@ -499,6 +537,22 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
     if (D.kind == CK_LAYER_POOL) {
       L.arg_off = a_cursor;
       a_cursor = align32(a_cursor + L.cells);
+      if (k > 0 && N.L[k - 1].kind == L_CONV) {   // compact winner data for the sparse backward
+        LayerDev& C = N.L[k - 1];
+        C.pool_above = C.has_delta;
+        // weight_grad lane layout: tap-major (lanes = taps x groups walking
+        // the winners) or winner-major (lanes walk winners, per-tap partials
+        // + xor trees); pick the cheaper one for this geometry
+        const int kk = C.kx * C.ky, phw = D.width * D.height;
+        const int G = kk >= 32 ? 1 : std::min(32 / kk, phw);
+        const int cost_tap = ((phw + G - 1) / G) * 6 * ((kk + 31) / 32);
+        const int cost_win = ((phw + 31) / 32) * kk * 3 + kk * 15;
+        C.wg_winner_major = C.kx == C.ky && C.kx >= 2 && C.kx <= 5 && cost_win < cost_tap;
+        L.wrc_off = a_cursor;
+        a_cursor = align32(a_cursor + L.cells);
+        L.wd_off = a_cursor;
+        a_cursor = align32(a_cursor + L.cells);
+      }
     }
     std::string where = "layer " + std::to_string(k) + ": ";
     switch (D.kind) {
@@ -564,6 +618,11 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
         return set_error(CK_E_CONFIG, where + "unknown layer kind");
     }
   }
+  for (int k = 0; k < n_layers; ++k)   // work splits use 32-bit (n * team size) products
+    if (N.L[k].cells > (1 << 22) || N.L[k].n_par > (1 << 22)) {
+      delete net;
+      return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": more than 4M cells/params");
+    }
   N.n_classes = N.L[n_layers - 1].cells;
   if (N.n_classes > kScratchDoubles) {
     delete net;
@@ -728,12 +787,17 @@ int ck_net_destroy(ck_net* net) {
 
 int ck_net_set_team(ck_net* net, int kind, int ctas, int threads) {
   CK_CHECK(net, CK_E_CONFIG, "null net");
-  if (kind == CK_TEAM_AUTO) kind = CK_TEAM_CLUSTER;
+  if (kind == CK_TEAM_AUTO) {
+    net->team_kind = CK_TEAM_AUTO;
+    net->team_ctas = 0;
+    net->threads = 512;
+    return CK_OK;
+  }
   CK_CHECK(kind == CK_TEAM_CLUSTER || kind == CK_TEAM_GRID, CK_E_CONFIG, "unknown team kind");
   CK_CHECK(threads >= 32 && threads <= 512 && threads % 32 == 0, CK_E_CONFIG,
            "threads must be a multiple of 32 in [32, 512]");
-  CK_CHECK(ctas >= 1 && (kind == CK_TEAM_GRID || ctas <= 16), CK_E_CONFIG,
-           "cluster teams hold 1..16 CTAs");
+  CK_CHECK(ctas >= 1 && ctas <= 1024 && (kind == CK_TEAM_GRID || ctas <= 16), CK_E_CONFIG,
+           "cluster teams hold 1..16 CTAs, grid teams 1..1024");
   net->team_kind = kind;
   net->team_ctas = ctas;
   net->threads = threads;
@@ -742,9 +806,10 @@ int ck_net_set_team(ck_net* net, int kind, int ctas, int threads) {
 
 int ck_net_get_team(const ck_net* net, int* kind, int* ctas, int* threads) {
   CK_CHECK(net && kind && ctas && threads, CK_E_CONFIG, "null argument");
-  *kind = net->team_kind;
-  *ctas = net->team_ctas;
-  *threads = net->threads;
+  const TeamShape t = resolve_team(net, 1);   // what a single-net launch uses
+  *kind = t.kind;
+  *ctas = t.ctas;
+  *threads = t.threads;
   return CK_OK;
 }
 
@@ -951,9 +1016,11 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
   CK_CUDA_TRY(cudaSetDevice(net->device));
   const int np = net->h.prog[PROG_TRAIN].n_phases;
   *n_phases = np;
-  CK_CHECK(max_phases >= np, CK_E_DIMENSION, "phase buffer too small");
+  CK_CHECK(max_phases >= 2 * np, CK_E_DIMENSION, "phase buffer too small");
+  const int ctas = resolve_team(net, 1).ctas;
+  const int64_t stride = 1 + (int64_t)np * (1 + ctas);
   long long* d_prof = nullptr;
-  CK_CUDA_TRY(cudaMalloc((void**)&d_prof, sizeof(long long) * n * (np + 1)));
+  CK_CUDA_TRY(cudaMalloc((void**)&d_prof, sizeof(long long) * n * stride));
   Job job = empty_job(PROG_TRAIN);
   job.images = images;
   job.lut = lut;
@@ -965,7 +1032,7 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
   job.prof = d_prof;
   job.prof_images = n;
   int rc = launch_teams(&net, 1, job, net->stream);
-  std::vector<long long> h((size_t)n * (np + 1));
+  std::vector<long long> h((size_t)(n * stride));
   if (rc == CK_OK) {
     cudaError_t e = cudaMemcpyAsync(h.data(), d_prof, sizeof(long long) * h.size(),
                                     cudaMemcpyDeviceToHost, net->stream);
@@ -974,10 +1041,21 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
   }
   cudaFree(d_prof);
   if (rc) return rc;
+  // phase_ns[p]: slowest CTA's work (phase start -> its work end);
+  // phase_ns[np + p]: barrier latency (slowest work end -> barrier exit)
   for (int p = 0; p < np; ++p) {
-    long long sum = 0;
-    for (int64_t t = 0; t < n; ++t) sum += h[t * (np + 1) + p + 1] - h[t * (np + 1) + p];
-    phase_ns[p] = sum / n;
+    long long work = 0, bar = 0;
+    for (int64_t t = 0; t < n; ++t) {
+      const long long* r = h.data() + t * stride;
+      const long long start = p == 0 ? r[0] : r[1 + (p - 1) * (1 + ctas)];
+      const long long* ph = r + 1 + p * (1 + ctas);
+      long long wmax = start;
+      for (int c = 0; c < ctas; ++c) wmax = std::max(wmax, ph[1 + c]);
+      work += wmax - start;
+      bar += ph[0] - wmax;
+    }
+    phase_ns[p] = work / n;
+    phase_ns[np + p] = bar / n;
   }
   return CK_OK;
 }
@@ -987,7 +1065,7 @@ int ck_net_describe_program(const ck_net* net, int prog, char* buf, int cap) {
   CK_CHECK(prog >= 0 && prog < N_PROGS, CK_E_CONFIG, "unknown program");
   static const char* names[] = {"load_input", "imgproc", "conv_fwd", "pool_fwd", "fc_fwd",
                                 "zero_delta", "out_delta", "fc_bwd", "conv_bwd", "update",
-                                "fc_out"};
+                                "fc_out", "conv_pool"};
   const Program& P = net->h.prog[prog];
   std::string s;
   for (int ph = 0; ph < P.n_phases; ++ph) {

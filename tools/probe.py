@@ -44,6 +44,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--imgs", type=int, default=2000)
     ap.add_argument("--configs", default="C1,C2,C3,C4")
+    ap.add_argument("--teams", default="1,16,512;1,8,512;2,148,512;2,74,512")
     args = ap.parse_args()
     for name in args.configs.split(","):
         with warnings.catch_warnings():
@@ -53,7 +54,7 @@ def main():
         n = args.imgs if name in ("C1", "C2") else max(200, args.imgs // 10)
         data = ck.make_glyph_dataset(n, spec.n_classes, w, seed=1, channels=c)
         cfg = ck.TrainConfig(epochs=1, eta0=1e-3, seed=0)
-        teams = [(1, 16, 512), (1, 8, 512), (1, 16, 256), (2, 148, 512), (2, 74, 512)]
+        teams = [tuple(int(v) for v in t.split(",")) for t in args.teams.split(";")]
         for team in teams:
             try:
                 net = ck.NetworkState(spec, 0, team=team)
@@ -64,10 +65,13 @@ def main():
                 net.close()
             except Exception as exc:  # keep probing other shapes
                 print(f"{name} team={team} failed: {exc}", flush=True)
-        net = ck.NetworkState(spec, 0)
-        print(net.describe_program(0), flush=True)
-        ph = ck.training.profile_phases(net, data.limit(200))
-        print(f"{name} phase ns:", ph.tolist(), "sum", int(ph.sum()), flush=True)
+        for team in ((1, 16, 512), (2, 148, 512)):
+            net = ck.NetworkState(spec, 0, team=team)
+            if team[0] == 1:
+                print(net.describe_program(0), flush=True)
+            work, bar = ck.training.profile_phases(net, data.limit(200))
+            print(f"{name} team={team} work ns:", work.tolist(), "sum", int(work.sum()),
+                  "| barrier ns:", bar.tolist(), "sum", int(bar.sum()), flush=True)
         ck.predict_batch(net, data.limit(10))
         ms = timed(lambda: ck.predict_batch(net, data))
         print(f"{name} eval: {ms:.2f} ms / {n} -> {n / ms * 1e3:.0f} img/s", flush=True)
