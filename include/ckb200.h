@@ -209,6 +209,11 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
  * 4 eval) for diagnostics and DESIGN.md. */
 int ck_net_describe_program(const ck_net* net, int prog, char* buf, int cap);
 
+/* Development aid: arm per-phase sub-timers of the training kernel.  Thread
+ * 0 of team rank `rank` writes %globaltimer at numbered points into
+ * dev_buf[phase * 32 + point] (>= 32 * n_phases int64, device); NULL disarms. */
+int ck_debug_subprof(long long* dev_buf, int rank);
+
 #ifdef __cplusplus
 }
 #endif

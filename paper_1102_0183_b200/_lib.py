@@ -14,7 +14,8 @@ import threading
 from .errors import CK_OK, StateError, error_for_status
 
 LIB_NAME = "libckb200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("CKB200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)   # override: experiments only
 
 _i32 = C.c_int
 _i64 = C.c_int64
@@ -83,6 +84,7 @@ _SIGNATURES = {
     "ck_net_profile_epoch": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _f64, _vp, _i32,
                                     C.POINTER(_i32)]),
     "ck_net_describe_program": (_i32, [_vp, _i32, C.c_char_p, _i32]),
+    "ck_debug_subprof": (_i32, [_vp, _i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

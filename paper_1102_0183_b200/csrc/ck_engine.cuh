@@ -49,10 +49,13 @@ struct LayerDev {
   int max_fan_in;                  // conv: largest forward row
   int pool_above;                  // conv: the next layer is a max-pool (sparse backward)
   int wg_winner_major;             // conv: sparse weight_grad splits winners over lanes
+  int wg_split;                    // conv: winner chunks per pair (one warp each)
+  int pull_g, pull_ch;             // conv: pull lane groups per warp, backward-list chunks
   int64_t p_off, b_off, n_par;     // params: conv arena / FC W, FC bias, count
   int64_t y_off, a_off, d_off, arg_off;  // act arena offsets (elements)
   int64_t wrc_off, wd_off;         // pool over a conv: winner (r<<16|c), winner delta
-  const int* fwd_off;              // conv tables (device, int32)
+  const int* fwd_off;              // conv tables (device, int32; read-only for a launch,
+                                   // always read with __ldg so they stay cached across barriers)
   const int* fwd_src;
   const int* fwd_widx;
   const int* bias_off;
@@ -143,14 +146,33 @@ struct Ctx {
 
 // Where this thread sits in its team, plus the CTA's shared scratch.
 struct TeamCtx {
+  int ph;                  // current phase (sub-phase timers)
   int rank, size;          // CTA rank in the team / CTAs in the team
   int gtid, gsize;         // thread index / count over the team
   int gwarp, gwarps;       // warp index / count over the team
   float* smem;             // per-CTA scratch
   int smem_floats;
+  // the current image (set per image by the kernel): bytes + LUT, or f32
+  const uint8_t* in_u8;
+  const float* in_lut;
+  const float* in_f32;
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Development timers (ck_debug_subprof): when armed, thread 0 of team rank
+// c_sub_rank records %globaltimer at numbered points of every phase into
+// c_sub[phase * 32 + point] (last image wins).  Unarmed cost: one constant load.
+__constant__ long long* c_sub;
+__constant__ int c_sub_rank;
+#define CK_SUBT(tm, i)                                                        \
+  do {                                                                        \
+    if (c_sub && threadIdx.x == 0 && (tm).rank == c_sub_rank) {               \
+      long long _t;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                  \
+      c_sub[(tm).ph * 32 + (i)] = _t;                                         \
+    }                                                                         \
+  } while (0)
 
 // Work split: items [0, n) are cut into one contiguous, balanced range per
 // CTA of the team; threads (or warps) stride inside their CTA's range.
@@ -187,6 +209,45 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void stage_sync() {
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+}
+
+// Copy n floats into the CTA's scratch when they fit (and n <= max_n), else
+// keep reading global memory.
+__device__ __forceinline__ const float* stage(const float* src, int n, const TeamCtx& tm,
+                                              int& used, int max_n = 1 << 30) {
+  if (n > max_n || used + n > tm.smem_floats) return src;
+  float* dst = tm.smem + used;
+  int head = 0;
+  if (((reinterpret_cast<uintptr_t>(src) ^ reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    head = (int)(((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) >> 2);
+    if (head > n) head = n;
+    const int n4 = (n - head) >> 2;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x)
+      cp_async16(dst + head + 4 * i, src + head + 4 * i);
+    for (int i = head + (n4 << 2) + threadIdx.x; i < n; i += blockDim.x)
+      cp_async4(dst + i, src + i);
+  } else {
+    head = n;
+  }
+  for (int i = threadIdx.x; i < head; i += blockDim.x) cp_async4(dst + i, src + i);
+  used += (n + 3) & ~3;
+  return dst;
+}
+
+// The current image's input values in the CTA's scratch, read straight from
+// the dataset (bytes through the LUT, or f32), so the first layer does not
+// wait a phase for OP_LOAD_INPUT to publish them.  nullptr if they do not fit.
+__device__ __forceinline__ const float* stage_input(const NetDev& N, const TeamCtx& tm,
+                                                    int& used) {
+  const int n = N.in_cells;
+  if (used + n > tm.smem_floats) return nullptr;
+  float* dst = tm.smem + used;
+  if (tm.in_u8) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(tm.in_lut + __ldg(tm.in_u8 + i));
+    used += (n + 3) & ~3;
+    return dst;
+  }
+  return stage(tm.in_f32, n, tm, used);
 }
 
 // ---------------------------------------------------------------------------
@@ -243,8 +304,12 @@ __device__ __forceinline__ void op_load_input(const NetDev& N, const Job& job,
 // One warp per output cell: lanes split the taps, fixed-order xor reduction.
 __device__ __forceinline__ void op_imgproc(const NetDev& N, const LayerDev& L, float* act,
                                            const TeamCtx& tm) {
+  __syncthreads();   // scratch reuse
   const LayerDev& I = N.L[0];
-  const float* src = act + I.y_off;
+  int used = 0;
+  const float* src = stage_input(N, tm, used);
+  if (!src) src = act + I.y_off;   // (never: the builder folds only inputs that fit)
+  stage_sync();
   float* out = act + L.y_off;
   const int hw = L.h * L.w;
   const int C = I.maps;
@@ -267,7 +332,7 @@ __device__ __forceinline__ void op_imgproc(const NetDev& N, const LayerDev& L, f
       const int i = t / L.fw, j = t % L.fw;
       const int yy = min(max(y + i - cy, 0), L.h - 1);
       const int xx = min(max(x + j - cx, 0), L.w - 1);
-      acc = __dadd_rn(acc, __dmul_rn(k[t], (double)s[yy * L.w + xx]));
+      acc = __dadd_rn(acc, __dmul_rn(__ldg(k + t), (double)s[yy * L.w + xx]));
     }
     acc = warp_sum(acc);
     if (lane == 0) out[q] = (float)acc;
@@ -320,10 +385,10 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   if (q0 >= q1) return;
   const int d0 = q0 / hw, d1 = (q1 - 1) / hw;
   const int kk = L.kx * L.ky;
-  const int k0 = L.fwd_off[d0], k1 = L.fwd_off[d1 + 1];
+  const int k0 = __ldg(L.fwd_off + (d0)), k1 = __ldg(L.fwd_off + (d1 + 1));
   const float* arena = N.params + L.p_off;
-  const int w0 = L.fwd_widx[k0];                      // first weight of map d0
-  const int n_w = L.bias_off[d1] + 1 - w0;            // through d1's bias
+  const int w0 = __ldg(L.fwd_widx + (k0));                      // first weight of map d0
+  const int n_w = __ldg(L.bias_off + (d1)) + 1 - w0;            // through d1's bias
   const int n_src = S.cells;
 
   // shared layout: [src offsets (k1-k0 ints)] [weights n_w] [source layer]
@@ -333,7 +398,7 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   const bool w_in_smem = (k1 - k0) + n_w <= tm.smem_floats;
   const bool s_in_smem = w_in_smem && (k1 - k0) + n_w + n_src <= tm.smem_floats;
   const float* src_g = act + S.y_off;
-  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = L.fwd_src[k0 + k] * (S.h * S.w);
+  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = __ldg(L.fwd_src + (k0 + k)) * (S.h * S.w);
   if (w_in_smem)
     for (int i = threadIdx.x; i < n_w; i += blockDim.x) cp_async4(ws + i, arena + w0 + i);
   if (s_in_smem)
@@ -349,15 +414,15 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const int d = q / hw, pix = q % hw;
     const int r = pix / L.w, c = pix % L.w;
-    const int kb = L.fwd_off[d], ke = L.fwd_off[d + 1];
-    const float* w = wbase + (L.fwd_widx[kb] - w0);
+    const int kb = __ldg(L.fwd_off + (d)), ke = __ldg(L.fwd_off + (d + 1));
+    const float* w = wbase + (__ldg(L.fwd_widx + (kb)) - w0);
     float acc = w[(ke - kb) * kk];                    // bias slot follows the blocks
     const int rc = (r * L.ty) * S.w + c * L.tx;
     if (offs) {
       acc = conv_cell<KX, KY>(acc, sbase + rc, offs + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
     } else {
       for (int k = kb; k < ke; ++k) {
-        const int so = L.fwd_src[k] * (S.h * S.w);
+        const int so = __ldg(L.fwd_src + (k)) * (S.h * S.w);
         acc = conv_cell<KX, KY>(acc, sbase + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
       }
     }
@@ -409,29 +474,6 @@ __device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L, 
   }
 }
 
-// Copy n floats into the CTA's scratch when they fit (and n <= max_n), else
-// keep reading global memory.
-__device__ __forceinline__ const float* stage(const float* src, int n, const TeamCtx& tm,
-                                              int& used, int max_n = 1 << 30) {
-  if (n > max_n || used + n > tm.smem_floats) return src;
-  float* dst = tm.smem + used;
-  int head = 0;
-  if (((reinterpret_cast<uintptr_t>(src) ^ reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-    head = (int)(((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) >> 2);
-    if (head > n) head = n;
-    const int n4 = (n - head) >> 2;
-    for (int i = threadIdx.x; i < n4; i += blockDim.x)
-      cp_async16(dst + head + 4 * i, src + head + 4 * i);
-    for (int i = head + (n4 << 2) + threadIdx.x; i < n; i += blockDim.x)
-      cp_async4(dst + i, src + i);
-  } else {
-    head = n;
-  }
-  for (int i = threadIdx.x; i < head; i += blockDim.x) cp_async4(dst + i, src + i);
-  used += (n + 3) & ~3;
-  return dst;
-}
-
 // ---------------------------------------------------------------------------
 // conv forward fused with the max-pool above it (kernels.py:70-87 then
 // :154-172).  Work is split by POOLED cells: a CTA computes every conv cell
@@ -446,12 +488,12 @@ __device__ __forceinline__ float conv_value_global(const LayerDev& L, const Laye
                                                    const float* arena, const float* src,
                                                    int d, int r, int c) {
   const int kk = L.kx * L.ky;
-  const int kb = L.fwd_off[d], ke = L.fwd_off[d + 1];
-  const float* w = arena + L.fwd_widx[kb];
-  float acc = arena[L.bias_off[d]];
+  const int kb = __ldg(L.fwd_off + (d)), ke = __ldg(L.fwd_off + (d + 1));
+  const float* w = arena + __ldg(L.fwd_widx + (kb));
+  float acc = arena[__ldg(L.bias_off + (d))];
   const int rc = (r * L.ty) * S.w + c * L.tx;
   for (int k = kb; k < ke; ++k) {
-    const int so = L.fwd_src[k] * (S.h * S.w);
+    const int so = __ldg(L.fwd_src + (k)) * (S.h * S.w);
     acc = conv_cell<KX, KY>(acc, src + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
   }
   return acc;
@@ -472,14 +514,22 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
   float* pyv = act + P.y_off;
   int* parg = reinterpret_cast<int*>(act + P.arg_off);
   int* pwrc = reinterpret_cast<int*>(act + P.wrc_off);
+  CK_SUBT(tm, 1);
   const Span sp = cta_span(P.cells, tm);
   int used = 0;
   const float* src_g = act + S.y_off;
   const float* src = src_g;
-  if (sp.b < sp.e && S.cells <= tm.smem_floats / 2) {
+  if (li == 1) {
+    if (sp.b < sp.e) {
+      const float* si = stage_input(N, tm, used);
+      if (si) src = si;
+    }
+  } else if (sp.b < sp.e && S.cells <= tm.smem_floats / 2) {
     // the whole source layer, unless this CTA's maps connect to fewer cells
-    const int nk_all = L.fwd_off[(sp.e - 1) / phw + 1] - L.fwd_off[sp.b / phw];
+    const int nk_all = __ldg(L.fwd_off + ((sp.e - 1) / phw + 1)) - __ldg(L.fwd_off + (sp.b / phw));
+    CK_SUBT(tm, 20);
     if (S.cells <= nk_all * shw) src = stage(src, S.cells, tm, used);
+    CK_SUBT(tm, 21);
   }
   const bool whole = src != src_g;
   const bool zero = full && (flags & F_ZERO_SELF);
@@ -492,10 +542,11 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
     // source map too -- sparse tables need far less than the whole layer)
     const int avail = tm.smem_floats - used;
     int qe = min(sp.e, q + avail / blk);
+    CK_SUBT(tm, 22);
     bool wst = false, slots = false;
     for (int tries = 0; tries < 24; ++tries) {
       const int d0 = q / phw, d1 = (qe - 1) / phw;
-      const int nk = L.fwd_off[d1 + 1] - L.fwd_off[d0];
+      const int nk = __ldg(L.fwd_off + (d1 + 1)) - __ldg(L.fwd_off + (d0));
       const int nw = nk * kk + d1 + 1 - d0;
       const int base = ((nk + 3) & ~3) + ((nw + 3) & ~3) + (qe - q) * blk;
       if (!whole && base + nk * shw <= avail) { wst = slots = true; break; }
@@ -506,8 +557,9 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       }
       qe = q + max(phw, (qe - q) / 2);
     }
+    CK_SUBT(tm, 2);
     const int d0 = q / phw, d1 = (qe - 1) / phw;
-    const int k0 = L.fwd_off[d0], k1 = L.fwd_off[d1 + 1];
+    const int k0 = __ldg(L.fwd_off + (d0)), k1 = __ldg(L.fwd_off + (d1 + 1));
     const int w0 = k0 * kk + d0;
     const int nw = (k1 - k0) * kk + d1 + 1 - d0;
     int* soff = reinterpret_cast<int*>(tm.smem + used);
@@ -519,12 +571,16 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       int u2 = used + ((k1 - k0 + 3) & ~3);
       stage(arena + w0, nw, tm, u2);
       for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x)
-        soff[k] = slots ? k * shw : L.fwd_src[k0 + k] * shw;
+        soff[k] = slots ? k * shw : __ldg(L.fwd_src + (k0 + k)) * shw;
       if (slots)
-        for (int e = threadIdx.x; e < (k1 - k0) * shw; e += blockDim.x)
-          cp_async4(sslot + e, src_g + L.fwd_src[k0 + e / shw] * shw + e % shw);
+        for (int k = (threadIdx.x >> 5); k < k1 - k0; k += (blockDim.x >> 5)) {
+          const float* from = src_g + __ldg(L.fwd_src + (k0 + k)) * shw;
+          for (int i = lane_id(); i < shw; i += 32) cp_async4(sslot + k * shw + i, from + i);
+        }
     }
+    CK_SUBT(tm, 3);
     stage_sync();
+    CK_SUBT(tm, 4);
     const int n_items = (qe - q) * blk;
     for (int it = threadIdx.x; it < n_items; it += blockDim.x) {
       const int qq = q + it / blk, t = it % blk;
@@ -533,7 +589,7 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       const int c = (pp % P.w) * P.px + t % P.px;
       float acc;
       if (wst) {
-        const int kb = L.fwd_off[d], ke = L.fwd_off[d + 1];
+        const int kb = __ldg(L.fwd_off + (d)), ke = __ldg(L.fwd_off + (d + 1));
         const float* w = ws + (kb * kk + d - w0);
         acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
                                 soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
@@ -547,7 +603,9 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       ybuf[it] = yv;
       if (zero) dl[cell] = 0.0f;
     }
+    CK_SUBT(tm, 5);
     __syncthreads();
+    CK_SUBT(tm, 6);
     for (int qi = threadIdx.x; qi < qe - q; qi += blockDim.x) {
       const float* yb = ybuf + qi * blk;
       int bt = 0;
@@ -563,6 +621,7 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       pwrc[qq] = (r << 16) | c;
     }
     __syncthreads();
+    CK_SUBT(tm, 7);
     q = qe;
   }
   if (full) {   // cells outside every pool block (rows / columns the pool drops)
@@ -576,7 +635,7 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
         int r, c;
         if (k < strip) { r = k / (L.w - cw); c = cw + k % (L.w - cw); }
         else { r = rh + (k - strip) / L.w; c = (k - strip) % L.w; }
-        const float acc = conv_value_global<KX, KY>(L, S, arena, act + S.y_off, d, r, c);
+        const float acc = conv_value_global<KX, KY>(L, S, arena, whole ? src : src_g, d, r, c);
         const int cell = d * hw + r * L.w + c;
         a[cell] = acc;
         y[cell] = conv_act(acc);
@@ -642,9 +701,15 @@ __device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, fl
   for (int tile = tm.rank; tile < n_tiles; tile += tm.size) {
     const int j0 = tile * kFcTile;
     const int nc = min(kFcTile, n_out - j0);
-    if (wst)
-      for (int e = threadIdx.x; e < n_in * nc; e += blockDim.x)
-        cp_async4(wt + (e / nc) * nc + e % nc, W + (int64_t)(e / nc) * n_out + j0 + e % nc);
+    if (wst) {
+      if (nc == kFcTile) {
+        for (int e = threadIdx.x; e < n_in * kFcTile; e += blockDim.x)
+          cp_async4(wt + e, W + (e / kFcTile) * n_out + j0 + e % kFcTile);
+      } else {
+        for (int e = threadIdx.x; e < n_in * nc; e += blockDim.x)
+          cp_async4(wt + e, W + (e / nc) * n_out + j0 + e % nc);
+      }
+    }
     stage_sync();
     fc_cols_preact(x, wst ? wt : W + j0, wst ? nc : n_out, N.params + L.b_off + j0, n_in, nc,
                    red, out_a);
@@ -788,9 +853,9 @@ __device__ __forceinline__ void wgrad_pair(const LayerDev& L, const LayerDev& S,
                                            float* g, bool upd, float eta_f) {
   const int lane = lane_id();
   const int hw = L.h * L.w;
-  const float* d = dl + L.pair_dst[p] * hw;
-  const float* s = ys + L.fwd_src[p] * (S.h * S.w);
-  const int o = L.fwd_widx[p];
+  const float* d = dl + __ldg(L.pair_dst + (p)) * hw;
+  const float* s = ys + __ldg(L.fwd_src + (p)) * (S.h * S.w);
+  const int o = __ldg(L.fwd_widx + (p));
   if constexpr (KX > 0) {
     constexpr int KK = KX * KY;
     double part[KK];
@@ -846,19 +911,29 @@ __device__ __forceinline__ void wgrad_pair(const LayerDev& L, const LayerDev& S,
 //   pull_bwd     one thread per source cell: for every dest map in its
 //                backward list, the pool blocks that meet the covering window,
 //                each contributing its winner when the winner lies inside
-// Tap-major: lane = (tap, group); a group walks every G-th winner of the
-// dest map; the groups are combined in group order.
+// Weight-gradient sums of one pair over the winners [wb, we) of its dest map.
+// Each function ends with the per-tap f64 sums; emit_wg either applies them
+// (out == nullptr: update in place or store the gradient) or parks them in
+// out[t] for a fixed-order combination with the pair's other winner chunks.
 //   wr / wdd  winner (r<<16|c) and winner delta of the pair's dest map
 //   s         the pair's source map (y of the layer below)
+__device__ __forceinline__ void emit_wg(int o, int t, double sum, double* out, float* arena,
+                                        float* g, bool upd, float eta_f) {
+  if (out) out[t] = sum;
+  else if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)sum);
+  else g[o + t] = (float)sum;
+}
+
+// Tap-major: lane = (tap, group); group gr walks winners wb+gr, wb+gr+G, ...;
+// the groups are combined in group order.
 __device__ __forceinline__ void wgrad_pair_sparse(const LayerDev& L, const LayerDev& S,
-                                                  const LayerDev& P, int o, const int* wr,
-                                                  const float* wdd, const float* s,
-                                                  float* arena, float* g, bool upd,
-                                                  float eta_f) {
+                                                  int o, const int* wr, const float* wdd,
+                                                  const float* s, int wb, int we,
+                                                  double* out, float* arena, float* g,
+                                                  bool upd, float eta_f) {
   const int lane = lane_id();
   const int kk = L.kx * L.ky;
-  const int phw = P.h * P.w;
-  const int G = kk >= 32 ? 1 : min(32 / kk, phw);
+  const int G = kk >= 32 ? 1 : 32 / kk;
   for (int t0 = 0; t0 < kk; t0 += 32) {
     const int t = kk >= 32 ? t0 + lane : lane % kk;
     const int grp = kk >= 32 ? 0 : lane / kk;
@@ -866,17 +941,15 @@ __device__ __forceinline__ void wgrad_pair_sparse(const LayerDev& L, const Layer
     if (t < kk && grp < G) {
       const int v = t / L.kx, u = t % L.kx;
       const float* sv = s + v * S.w + u;
-      for (int wq = grp; wq < phw; wq += G) {
+#pragma unroll 4
+      for (int wq = wb + grp; wq < we; wq += G) {
         const int rc = wr[wq];
         part += (double)__fmul_rn(wdd[wq], sv[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx]);
       }
     }
     double tot = part;
     for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, part, (lane + gg * kk) & 31);
-    if (grp == 0 && t < kk) {
-      if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)tot);
-      else g[o + t] = (float)tot;
-    }
+    if (grp == 0 && t < kk) emit_wg(o, t, tot, out, arena, g, upd, eta_f);
   }
 }
 
@@ -884,17 +957,16 @@ __device__ __forceinline__ void wgrad_pair_sparse(const LayerDev& L, const Layer
 // each lane keeps kx*ky f64 partials, then one fixed xor tree per tap.
 template <int KX, int KY>
 __device__ __forceinline__ void wgrad_pair_winners(const LayerDev& L, const LayerDev& S,
-                                                   const LayerDev& P, int o, const int* wr,
-                                                   const float* wdd, const float* s,
-                                                   float* arena, float* g, bool upd,
-                                                   float eta_f) {
+                                                   int o, const int* wr, const float* wdd,
+                                                   const float* s, int wb, int we,
+                                                   double* out, float* arena, float* g,
+                                                   bool upd, float eta_f) {
   constexpr int KK = KX * KY;
   const int lane = lane_id();
-  const int phw = P.h * P.w;
   double part[KK];
 #pragma unroll
   for (int t = 0; t < KK; ++t) part[t] = 0.0;
-  for (int wq = lane; wq < phw; wq += 32) {
+  for (int wq = wb + lane; wq < we; wq += 32) {
     const int rc = wr[wq];
     const float dv = wdd[wq];
     const float* base = s + (rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx;
@@ -904,24 +976,21 @@ __device__ __forceinline__ void wgrad_pair_winners(const LayerDev& L, const Laye
 #pragma unroll
   for (int t = 0; t < KK; ++t) {
     const double sum = warp_sum(part[t]);
-    if (lane == t % 32) {
-      if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)sum);
-      else g[o + t] = (float)sum;
-    }
+    if (lane == t % 32) emit_wg(o, t, sum, out, arena, g, upd, eta_f);
   }
 }
 
-__device__ __forceinline__ void wgrad_sparse(const LayerDev& L, const LayerDev& S,
-                                             const LayerDev& P, int o, const int* wr,
-                                             const float* wdd, const float* s, float* arena,
+__device__ __forceinline__ void wgrad_sparse(const LayerDev& L, const LayerDev& S, int o,
+                                             const int* wr, const float* wdd, const float* s,
+                                             int wb, int we, double* out, float* arena,
                                              float* g, bool upd, float eta_f) {
   if (L.wg_winner_major) {
-    if (L.kx == 2 && L.ky == 2) return wgrad_pair_winners<2, 2>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
-    if (L.kx == 3 && L.ky == 3) return wgrad_pair_winners<3, 3>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
-    if (L.kx == 4 && L.ky == 4) return wgrad_pair_winners<4, 4>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
-    if (L.kx == 5 && L.ky == 5) return wgrad_pair_winners<5, 5>(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+    if (L.kx == 2 && L.ky == 2) return wgrad_pair_winners<2, 2>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
+    if (L.kx == 3 && L.ky == 3) return wgrad_pair_winners<3, 3>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
+    if (L.kx == 4 && L.ky == 4) return wgrad_pair_winners<4, 4>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
+    if (L.kx == 5 && L.ky == 5) return wgrad_pair_winners<5, 5>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
   }
-  wgrad_pair_sparse(L, S, P, o, wr, wdd, s, arena, g, upd, eta_f);
+  wgrad_pair_sparse(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
 }
 
 // Each CTA stages exactly what its share needs (one cp.async round trip per
@@ -948,6 +1017,8 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
   const float* wd_g = act + P.wd_off;
   const float* ys_g = act + S.y_off;
   const int cap = tm.smem_floats - 16;
+  const int split = L.wg_split;
+  CK_SUBT(tm, 10);
 
   // ---- weight gradients
   const int n_w = L.n_pairs;
@@ -956,9 +1027,10 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
   for (int c0 = ts.b; c0 < p1;) {
     int c1 = p1, da, db, need;
     for (;;) {
-      da = L.pair_dst[c0];
-      db = L.pair_dst[c1 - 1];
-      need = 2 * (db - da + 1) * phw + (c1 - c0) * shw + 8;
+      da = __ldg(L.pair_dst + (c0));
+      db = __ldg(L.pair_dst + (c1 - 1));
+      need = 2 * (db - da + 1) * phw + (c1 - c0) * shw + 8 +
+             (split > 1 ? 2 * (c1 - c0) * split * kk + 4 : 0);
       if (need <= cap || c1 - c0 == 1) break;
       c1 = c0 + (c1 - c0) / 2;
     }
@@ -972,18 +1044,41 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
           stage(reinterpret_cast<const float*>(wr), (db - da + 1) * phw, tm, used));
       wdd = stage(wdd, (db - da + 1) * phw, tm, used);
       slots = tm.smem + used;
-      for (int e = threadIdx.x; e < (c1 - c0) * shw; e += blockDim.x) {
-        const int p = c0 + e / shw;
-        cp_async4(slots + e, ys_g + L.fwd_src[p] * shw + e % shw);
+      for (int p = c0 + warp; p < c1; p += nwarps) {   // one warp per pair's source map
+        const float* from = ys_g + __ldg(L.fwd_src + (p)) * shw;
+        float* to = slots + (p - c0) * shw;
+        for (int i = lane; i < shw; i += 32) cp_async4(to + i, from + i);
       }
     }
+    CK_SUBT(tm, 11);
     stage_sync();
-    for (int p = c0 + warp; p < c1; p += nwarps) {
-      const int off = (L.pair_dst[p] - da) * phw;
-      const float* sp = fits ? slots + (p - c0) * shw : ys_g + L.fwd_src[p] * shw;
-      wgrad_sparse(L, S, P, L.fwd_widx[p], wr + off, wdd + off, sp, arena, g, upd, eta_f);
+    CK_SUBT(tm, 12);
+    // task = (pair, winner chunk); chunk partials are combined in chunk order
+    double* parts = nullptr;
+    if (split > 1) {
+      const int after = fits ? used + (c1 - c0) * shw : 0;
+      parts = reinterpret_cast<double*>(tm.smem + ((after + 3) & ~3));
     }
+    for (int task = warp; task < (c1 - c0) * split; task += nwarps) {
+      const int p = c0 + task / split, ch = task % split;
+      const int off = (__ldg(L.pair_dst + (p)) - da) * phw;
+      const float* sp = fits ? slots + (p - c0) * shw : ys_g + __ldg(L.fwd_src + (p)) * shw;
+      wgrad_sparse(L, S, __ldg(L.fwd_widx + (p)), wr + off, wdd + off, sp, ch * phw / split,
+                   (ch + 1) * phw / split, parts ? parts + task * kk : nullptr, arena, g,
+                   upd, eta_f);
+    }
+    CK_SUBT(tm, 13);
     __syncthreads();
+    if (split > 1) {
+      for (int e = threadIdx.x; e < (c1 - c0) * kk; e += blockDim.x) {
+        const int pi = e / kk, t = e % kk;
+        double sum = 0.0;
+        for (int ch = 0; ch < split; ++ch) sum += parts[(pi * split + ch) * kk + t];
+        emit_wg(__ldg(L.fwd_widx + (c0 + pi)), t, sum, nullptr, arena, g, upd, eta_f);
+      }
+      __syncthreads();
+    }
+    CK_SUBT(tm, 14);
     c0 = c1;
   }
   // ---- bias gradients: one warp per dest map
@@ -993,58 +1088,65 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
     for (int wq = lane; wq < phw; wq += 32) acc += (double)wd_g[d * phw + wq];
     acc = warp_sum(acc);
     if (lane == 0) {
-      const int o = L.bias_off[d];
+      const int o = __ldg(L.bias_off + (d));
       if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
       else g[o] = (float)acc;
     }
   }
+  CK_SUBT(tm, 15);
   if (!(flags & F_PULL)) {
     __syncthreads();
     return;
   }
 
-  // ---- pull: kPullLanes lanes per source cell; lane l walks the backward
-  // list entries l, l + kPullLanes, ...; partials combined by a fixed xor tree
-  const Span cs = cta_span(S.cells, tm);
-  const int grp = threadIdx.x / kPullLanes, sub = threadIdx.x % kPullLanes;
-  const unsigned gmask = ((1u << kPullLanes) - 1) << (lane & ~(kPullLanes - 1));
-  const int per_k = kk + 2 * phw;
-  for (int cell0 = cs.b; cell0 < cs.e;) {
-    const int sa = cell0 / shw;
-    int sb = (cs.e - 1) / shw;
-    int ka = L.bwd_off[sa], kb = L.bwd_off[sb + 1];
-    while ((kb - ka) * per_k > cap && sb > sa) {
-      sb = sa + (sb - sa + 1) / 2 - 1;
-      kb = L.bwd_off[sb + 1];
+  // ---- pull, as a scatter per source map.  Every (dest entry, winner) adds
+  // delta_w * W[d,s,v,u] to source cell (r*ty+v, c*tx+u).  A stream (one lane
+  // group of one warp: lane = tap) owns a private f64 buffer of the source
+  // map, so the taps of one winner never collide; the layer's pull_ch chunks
+  // of the backward list times pull_g lane groups give a fixed set of streams,
+  // combined in stream order -- independent of the team.
+  const int G = L.pull_g, NCH = L.pull_ch, NS = NCH * G;
+  const Span ms = cta_span(S.maps, tm);
+  const int per_map = NS * shw * 2;                 // stream buffers (floats)
+  for (int m0 = ms.b; m0 < ms.e;) {
+    int m1 = min(ms.e, m0 + max(1, nwarps / NCH));
+    int ka = __ldg(L.bwd_off + (m0)), kb = __ldg(L.bwd_off + (m1));
+    while (m1 - m0 > 1 && (m1 - m0) * per_map + (kb - ka) * (kk + 2 * phw) > cap) {
+      --m1;
+      kb = __ldg(L.bwd_off + (m1));
     }
-    const int cell1 = min(cs.e, (sb + 1) * shw);
-    const bool fits = (kb - ka) * per_k <= cap;
-    float* wst = tm.smem;
-    int* wrs = reinterpret_cast<int*>(tm.smem + (kb - ka) * kk);
-    float* wds = tm.smem + (kb - ka) * (kk + phw);
+    const int bufs = (m1 - m0) * per_map;
+    const bool fits = bufs + (kb - ka) * (kk + 2 * phw) <= cap;
+    double* buf = reinterpret_cast<double*>(tm.smem);
+    float* wst = tm.smem + bufs;
+    int* wrs = reinterpret_cast<int*>(wst + (kb - ka) * kk);
+    float* wds = wst + (kb - ka) * (kk + phw);
+    for (int i = threadIdx.x; i < bufs / 2; i += blockDim.x) buf[i] = 0.0;
     if (fits) {
-      for (int e = threadIdx.x; e < (kb - ka) * kk; e += blockDim.x)
-        cp_async4(wst + e, arena + L.bwd_widx[ka + e / kk] + e % kk);
-      for (int e = threadIdx.x; e < (kb - ka) * phw; e += blockDim.x) {
-        const int src = L.bwd_dst[ka + e / phw] * phw + e % phw;
-        cp_async4(wrs + e, wrc_g + src);
-        cp_async4(wds + e, wd_g + src);
+      for (int k = ka + warp; k < kb; k += nwarps) {   // one warp per backward entry
+        const float* wfrom = arena + __ldg(L.bwd_widx + (k));
+        for (int i = lane; i < kk; i += 32) cp_async4(wst + (k - ka) * kk + i, wfrom + i);
+        const int d = __ldg(L.bwd_dst + (k));
+        for (int i = lane; i < phw; i += 32) {
+          cp_async4(wrs + (k - ka) * phw + i, wrc_g + d * phw + i);
+          cp_async4(wds + (k - ka) * phw + i, wd_g + d * phw + i);
+        }
       }
     }
+    CK_SUBT(tm, 16);
     stage_sync();
-    for (int cell = cell0 + grp; cell < cell1; cell += blockDim.x / kPullLanes) {
-      const int sm = cell / shw, pix = cell % shw;
-      const int j = pix / S.w, i = pix % S.w;
-      const int ylo = ceil_div_clamp0(j - L.ky + 1, L.ty);
-      const int yhi = min(j / L.ty, L.h - 1);
-      const int xlo = ceil_div_clamp0(i - L.kx + 1, L.tx);
-      const int xhi = min(i / L.tx, L.w - 1);
-      double acc = 0.0;
-      if (ylo <= yhi && xlo <= xhi) {
-        const int prlo = ylo / P.py, prhi = min(yhi / P.py, P.h - 1);
-        const int pclo = xlo / P.px, pchi = min(xhi / P.px, P.w - 1);
-        const int k1 = L.bwd_off[sm + 1];
-        for (int k = L.bwd_off[sm] + sub; k < k1; k += kPullLanes) {
+    CK_SUBT(tm, 17);
+    const int grp = kk >= 32 ? 0 : lane / kk;
+    for (int task = warp; task < (m1 - m0) * NCH; task += nwarps) {
+      const int mi = task / NCH, ch = task % NCH;
+      const int k0m = __ldg(L.bwd_off + (m0 + mi)), nkm = __ldg(L.bwd_off + (m0 + mi + 1)) - k0m;
+      const int kc0 = k0m + ch * nkm / NCH, kc1 = k0m + (ch + 1) * nkm / NCH;
+      for (int t0 = 0; t0 < kk; t0 += 32) {
+        const int t = kk >= 32 ? t0 + lane : lane % kk;
+        const bool on = t < kk && grp < G;
+        const int v = t / L.kx, u = t % L.kx;
+        double* acc = buf + ((mi * NCH + ch) * G + (on ? grp : 0)) * shw + v * S.w + u;
+        for (int k = kc0; k < kc1; ++k) {
           const float* wk;
           const int* wr;
           const float* wdd;
@@ -1053,27 +1155,36 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
             wr = wrs + (k - ka) * phw;
             wdd = wds + (k - ka) * phw;
           } else {
-            const int d = L.bwd_dst[k];
-            wk = arena + L.bwd_widx[k];
+            const int d = __ldg(L.bwd_dst + (k));
+            wk = arena + __ldg(L.bwd_widx + (k));
             wr = wrc_g + d * phw;
             wdd = wd_g + d * phw;
           }
-          for (int pr = prlo; pr <= prhi; ++pr)
-            for (int pc = pclo; pc <= pchi; ++pc) {
-              const int q = pr * P.w + pc;
+          const float wt = on ? wk[t] : 0.0f;
+          for (int q0 = 0; q0 < phw; q0 += G) {   // uniform rounds: group grp takes q0 + grp
+            const int q = q0 + grp;
+            if (on && q < phw) {
               const int rc = wr[q];
-              const int r = rc >> 16, c = rc & 0xffff;
-              if (r >= ylo && r <= yhi && c >= xlo && c <= xhi)
-                acc += (double)__fmul_rn(wdd[q], wk[(j - r * L.ty) * L.kx + (i - c * L.tx)]);
+              acc[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx] +=
+                  (double)__fmul_rn(wdd[q], wt);
             }
+            __syncwarp();
+          }
         }
       }
-#pragma unroll
-      for (int o = kPullLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
-      if (sub == 0) emit_delta(N, act, li - 1, cell, (float)acc);
+    }
+    CK_SUBT(tm, 18);
+    __syncthreads();
+    for (int e = threadIdx.x; e < (m1 - m0) * shw; e += blockDim.x) {
+      const int mi = e / shw, cell = e % shw;
+      const double* b = buf + mi * NS * shw + cell;
+      double sum = 0.0;
+      for (int st = 0; st < NS; ++st) sum += b[st * shw];
+      emit_delta(N, act, li - 1, (m0 + mi) * shw + cell, (float)sum);
     }
     __syncthreads();
-    cell0 = cell1;
+    CK_SUBT(tm, 19);
+    m0 = m1;
   }
 }
 
@@ -1111,7 +1222,7 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
       for (int i = lane; i < hw; i += 32) acc += (double)dd[i];
       acc = warp_sum(acc);
       if (lane == 0) {
-        const int o = L.bias_off[d];
+        const int o = __ldg(L.bias_off + (d));
         if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
         else g[o] = (float)acc;
       }
@@ -1132,18 +1243,18 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
       // cell, so four destinations share one loop nest: accumulator q takes
       // the destinations k = kb + q (mod 4), combined in fixed order.
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const int kb = L.bwd_off[s], k1 = L.bwd_off[s + 1];
+      const int kb = __ldg(L.bwd_off + (s)), k1 = __ldg(L.bwd_off + (s + 1));
       const int dw0 = (j - ylo * L.ty) * L.kx + i - xlo * L.tx;   // weight index at (ylo, xlo)
       int k = kb;
       for (; k + 4 <= k1; k += 4) {
-        const float* d0 = dl + L.bwd_dst[k] * hw + ylo * L.w;
-        const float* d1 = dl + L.bwd_dst[k + 1] * hw + ylo * L.w;
-        const float* d2 = dl + L.bwd_dst[k + 2] * hw + ylo * L.w;
-        const float* d3 = dl + L.bwd_dst[k + 3] * hw + ylo * L.w;
-        const float* w0 = arena + L.bwd_widx[k] + dw0;
-        const float* w1 = arena + L.bwd_widx[k + 1] + dw0;
-        const float* w2 = arena + L.bwd_widx[k + 2] + dw0;
-        const float* w3 = arena + L.bwd_widx[k + 3] + dw0;
+        const float* d0 = dl + __ldg(L.bwd_dst + (k)) * hw + ylo * L.w;
+        const float* d1 = dl + __ldg(L.bwd_dst + (k + 1)) * hw + ylo * L.w;
+        const float* d2 = dl + __ldg(L.bwd_dst + (k + 2)) * hw + ylo * L.w;
+        const float* d3 = dl + __ldg(L.bwd_dst + (k + 3)) * hw + ylo * L.w;
+        const float* w0 = arena + __ldg(L.bwd_widx + (k)) + dw0;
+        const float* w1 = arena + __ldg(L.bwd_widx + (k + 1)) + dw0;
+        const float* w2 = arena + __ldg(L.bwd_widx + (k + 2)) + dw0;
+        const float* w3 = arena + __ldg(L.bwd_widx + (k + 3)) + dw0;
         for (int y = ylo; y <= yhi; ++y) {
           for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx) {
             acc[0] += (double)__fmul_rn(d0[x], w0[wi]);
@@ -1156,8 +1267,8 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
         }
       }
       for (; k < k1; ++k) {
-        const float* d = dl + L.bwd_dst[k] * hw + ylo * L.w;
-        const float* w = arena + L.bwd_widx[k] + dw0;
+        const float* d = dl + __ldg(L.bwd_dst + (k)) * hw + ylo * L.w;
+        const float* w = arena + __ldg(L.bwd_widx + (k)) + dw0;
         double part = 0.0;
         for (int y = ylo; y <= yhi; ++y, d += L.w, w -= L.ty * L.kx)
           for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx)

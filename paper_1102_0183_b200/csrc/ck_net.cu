@@ -18,6 +18,10 @@
 #include "ck_engine.cuh"
 #include "ck_host.h"
 
+#ifndef CK_TEAM_THREADS
+#define CK_TEAM_THREADS 512
+#endif
+
 namespace ck {
 
 constexpr int kMaxNetsPerLaunch = 64;
@@ -81,6 +85,23 @@ struct GridTeam {
   }
 };
 
+// Point the team context at the current image (dataset bytes + LUT, f32
+// dataset, or the host-staged input already in the activation arena).
+__device__ __forceinline__ void set_input(const NetDev& N, const Job& job, const Ctx& ctx,
+                                          TeamCtx& tm) {
+  tm.in_u8 = nullptr;
+  tm.in_lut = nullptr;
+  if (job.images && job.lut) {
+    tm.in_u8 = job.images + ctx.img * (int64_t)N.in_cells;
+    tm.in_lut = job.lut;
+    tm.in_f32 = nullptr;
+  } else if (job.images) {
+    tm.in_f32 = reinterpret_cast<const float*>(job.images) + ctx.img * (int64_t)N.in_cells;
+  } else {
+    tm.in_f32 = ctx.act + N.L[0].y_off;
+  }
+}
+
 // Copy a net descriptor into shared memory (descriptor reads then never
 // touch L1/L2 inside the image loop).
 __device__ __forceinline__ void load_desc(NetDev* dst, const NetDev* src) {
@@ -105,7 +126,7 @@ constexpr int kTeamStageFloats = 48 * 1024;   // 192 KB staging per CTA
 constexpr int kEvalStageFloats = 12 * 1024;   // 48 KB staging per CTA
 
 template <class Team>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(CK_TEAM_THREADS, 1)
 net_team_kernel(NetPtrs nets, Job job, int ctas) {
   extern __shared__ __align__(16) unsigned char smem[];
   NetDev& N = *reinterpret_cast<NetDev*>(smem);
@@ -126,6 +147,7 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
 
   const Program& P = N.prog[job.prog];
   TeamCtx tm;
+  tm.ph = 0;
   tm.rank = rank;
   tm.size = tsize;
   tm.gtid = rank * blockDim.x + threadIdx.x;
@@ -144,18 +166,23 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
   unsigned bar_target = 0;
   for (int64_t t = 0; t < job.n; ++t) {
     ctx.t = t;
-    ctx.img = job.order ? (int64_t)job.order[t] : job.first + t;
-    ctx.label = job.labels ? job.labels[ctx.img] : -1;
+    ctx.img = job.order ? (int64_t)__ldg(job.order + t) : job.first + t;
+    ctx.label = job.labels ? __ldg(job.labels + ctx.img) : -1;
+    set_input(N, job, ctx, tm);
     long long* prof = (job.prof && team == 0 && t < job.prof_images)
                           ? job.prof + t * prof_stride : nullptr;
     if (prof && rank == 0 && threadIdx.x == 0) prof[0] = globaltimer();
     for (int ph = 0; ph < P.n_phases; ++ph) {
+      tm.ph = ph;
+      CK_SUBT(tm, 0);
       run_phase(N, P, ph, job, ctx, tm, scratch);
+      CK_SUBT(tm, 30);
       if (prof) {
         __syncthreads();
         if (threadIdx.x == 0) prof[1 + ph * (1 + tsize) + 1 + rank] = globaltimer();
       }
       Team::sync(N, ctas, bar_target);
+      CK_SUBT(tm, 31);
       if (prof && rank == 0 && threadIdx.x == 0) prof[1 + ph * (1 + tsize)] = globaltimer();
     }
     if (rank == 0 && threadIdx.x == 0 && job.prog != PROG_FORWARD && job.prog != PROG_APPLY) {
@@ -178,6 +205,7 @@ net_eval_kernel(const NetDev* net, Job job) {
   load_desc(&N, net);
   const Program& P = N.prog[PROG_EVAL];
   TeamCtx tm;
+  tm.ph = 0;
   tm.rank = 0;
   tm.size = 1;
   tm.gtid = threadIdx.x;
@@ -192,6 +220,7 @@ net_eval_kernel(const NetDev* net, Job job) {
   for (int64_t t = blockIdx.x; t < job.n; t += gridDim.x) {
     ctx.t = t;
     ctx.img = job.first + t;
+    set_input(N, job, ctx, tm);
     for (int ph = 0; ph < P.n_phases; ++ph) {
       run_phase(N, P, ph, job, ctx, tm, nullptr);
       __syncthreads();
@@ -280,11 +309,18 @@ struct ProgramBuilder {
 // `skip_out`: the output layer's forward is folded into OP_FC_OUT.
 void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero,
                    bool skip_out = false) {
-  if (load) {
+  const int last = skip_out ? N.n_layers - 1 : N.n_layers;
+  // The first layer can read the image itself (stage_input) when it is a
+  // conv+pool or the contrast layer and the image fits in shared memory; the
+  // input copy for later phases is then published in that same phase.
+  const bool fold = load && N.in_cells <= 8192 && N.n_layers > 2 &&
+                    ((N.L[1].kind == L_CONV && 2 < last && N.L[2].kind == L_POOL) ||
+                     N.L[1].kind == L_IMGPROC);
+  if (load && !fold) {
     b.add(OP_LOAD_INPUT, 0);
     b.phase();
   }
-  const int last = skip_out ? N.n_layers - 1 : N.n_layers;
+  if (fold) b.add(OP_LOAD_INPUT, 0);
   for (int k = 1; k < last; ++k) {
     const LayerDev& L = N.L[k];
     const bool scatter_target = zero && k + 1 < N.n_layers &&
@@ -543,11 +579,23 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
         // weight_grad lane layout: tap-major (lanes = taps x groups walking
         // the winners) or winner-major (lanes walk winners, per-tap partials
         // + xor trees); pick the cheaper one for this geometry
+        // maps with many winners split each pair's sum into wg_split chunks
+        // (one warp each, combined in chunk order: a geometry constant, so
+        // results never depend on the team)
         const int kk = C.kx * C.ky, phw = D.width * D.height;
-        const int G = kk >= 32 ? 1 : std::min(32 / kk, phw);
-        const int cost_tap = ((phw + G - 1) / G) * 6 * ((kk + 31) / 32);
-        const int cost_win = ((phw + 31) / 32) * kk * 3 + kk * 15;
+        C.wg_split = std::max(1, std::min(16, phw / 24));
+        const int chunk = (phw + C.wg_split - 1) / C.wg_split;
+        const int G = kk >= 32 ? 1 : std::min(32 / kk, chunk);
+        const int cost_tap = ((chunk + G - 1) / G) * 40 * ((kk + 31) / 32);
+        const int cost_win = ((chunk + 31) / 32) * kk * 3 + kk * 15;
         C.wg_winner_major = C.kx == C.ky && C.kx >= 2 && C.kx <= 5 && cost_win < cost_tap;
+        // pull streams: lane groups (one winner each, lane = tap) x chunks of
+        // the backward list, <= 16 f64 copies of a source map in shared memory
+        C.pull_g = kk >= 32 ? 1 : std::min(32 / kk, phw);
+        C.pull_ch = std::max(1, 16 / C.pull_g);
+        const int src_cells = N.L[k - 2].h * N.L[k - 2].w;
+        while (C.pull_ch > 1 && C.pull_ch * C.pull_g * src_cells * 2 > kTeamStageFloats / 2)
+          --C.pull_ch;
         L.wrc_off = a_cursor;
         a_cursor = align32(a_cursor + L.cells);
         L.wd_off = a_cursor;
@@ -1057,6 +1105,14 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
     phase_ns[p] = work / n;
     phase_ns[np + p] = bar / n;
   }
+  return CK_OK;
+}
+
+// Development aid (not in ckb200.h's stable surface): arm the sub-phase
+// timers with a device buffer of >= 32 * n_phases int64 (NULL disarms).
+int ck_debug_subprof(long long* dev_buf, int rank) {
+  CK_CUDA_TRY(cudaMemcpyToSymbol(c_sub, &dev_buf, sizeof(dev_buf)));
+  CK_CUDA_TRY(cudaMemcpyToSymbol(c_sub_rank, &rank, sizeof(rank)));
   return CK_OK;
 }
 
