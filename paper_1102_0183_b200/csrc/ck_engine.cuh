@@ -37,34 +37,39 @@ constexpr int kStageMax = 4096;    // largest per-layer array every CTA copies
 
 enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
 
+// Every field of a layer's geometry, in declaration order.  The geometry is
+// plain integers (tables are offsets into one int32 table block), so a whole
+// net can be a compile-time constant: the spec generator prints this list for
+// the specialised kernels (ck_specs.cuh).
+#define CK_LAYER_FIELDS(X)                                                   \
+  X(int, kind) X(int, maps) X(int, h) X(int, w) X(int, cells)                \
+  X(int, src_maps) X(int, src_h) X(int, src_w) X(int, src_cells)             \
+  X(int, kx) X(int, ky) X(int, tx) X(int, ty) X(int, px) X(int, py)          \
+  X(int, n_pairs) X(int, has_delta) X(int, n_filt) X(int, fh) X(int, fw)     \
+  X(int, max_fan_in) X(int, pool_above) X(int, wg_winner_major)              \
+  X(int, wg_split) X(int, pull_g) X(int, pull_ch)                            \
+  X(int64_t, p_off) X(int64_t, b_off) X(int64_t, n_par)                      \
+  X(int64_t, y_off) X(int64_t, a_off) X(int64_t, d_off) X(int64_t, arg_off)  \
+  X(int64_t, wrc_off) X(int64_t, wd_off)                                     \
+  X(int, o_fwd_off) X(int, o_fwd_src) X(int, o_fwd_widx) X(int, o_bias_off)  \
+  X(int, o_bwd_off) X(int, o_bwd_dst) X(int, o_bwd_widx) X(int, o_pair_dst)  \
+  X(int, o_filt)
+
+// Field notes: tx = sx + 1 (conv stride); pool_above: the next layer is a
+// max-pool (sparse backward); wg_*: weight-gradient lane layout / winner
+// chunks; pull_g / pull_ch: pull lane groups / backward-list chunks;
+// *_off: act-arena offsets (elements); wrc_off / wd_off: a pool over a conv
+// keeps winner (r<<16|c) and winner delta per pooled cell; o_*: offsets of
+// the conv tables (int32, read-only for a launch, always read with __ldg)
+// and of the contrast filter coefficients.
 struct LayerDev {
-  int kind;
-  int maps, h, w, cells;           // output geometry
-  int src_maps, src_h, src_w, src_cells;
-  int kx, ky, tx, ty;              // conv (tx = sx + 1)
-  int px, py;                      // pool
-  int n_pairs;
-  int has_delta;
-  int n_filt, fh, fw;              // imgproc
-  int max_fan_in;                  // conv: largest forward row
-  int pool_above;                  // conv: the next layer is a max-pool (sparse backward)
-  int wg_winner_major;             // conv: sparse weight_grad splits winners over lanes
-  int wg_split;                    // conv: winner chunks per pair (one warp each)
-  int pull_g, pull_ch;             // conv: pull lane groups per warp, backward-list chunks
-  int64_t p_off, b_off, n_par;     // params: conv arena / FC W, FC bias, count
-  int64_t y_off, a_off, d_off, arg_off;  // act arena offsets (elements)
-  int64_t wrc_off, wd_off;         // pool over a conv: winner (r<<16|c), winner delta
-  const int* fwd_off;              // conv tables (device, int32; read-only for a launch,
-                                   // always read with __ldg so they stay cached across barriers)
-  const int* fwd_src;
-  const int* fwd_widx;
-  const int* bias_off;
-  const int* bwd_off;
-  const int* bwd_dst;
-  const int* bwd_widx;
-  const int* pair_dst;
-  const double* filt;              // imgproc coefficients (n_filt, fh, fw)
+#define CK_DECL(t, n) t n;
+  CK_LAYER_FIELDS(CK_DECL)
+#undef CK_DECL
 };
+
+// table access: TB(L, fwd_off) -> const int* into the table block
+#define TB(L, f) (R.tables + (L).o_##f)
 
 enum OpKind {
   OP_LOAD_INPUT = 0,  // input y <- lut[image bytes] (no-op for host-staged x)
@@ -99,26 +104,34 @@ struct Program {
 enum ProgId { PROG_TRAIN = 0, PROG_FORWARD = 1, PROG_BACKWARD = 2, PROG_APPLY = 3,
               PROG_EVAL = 4, N_PROGS = 5 };
 
-struct NetDev {
+// A net's geometry and phase programs: plain values (compile-time constants
+// in the specialised kernels, a shared-memory copy in the generic ones).
+struct NetGeo {
   int n_layers;
   int n_classes;
   int in_cells;
   int pad0;
+  int64_t act_size;        // elements per act arena (one team)
+  LayerDev L[kMaxLayers];
+  Program prog[N_PROGS];
+};
+
+// A net's device memory.
+struct NetPtr {
   float* params;
   float* grads;
   float* act;
-  int64_t act_size;        // elements per act arena (one team)
-  unsigned* bar;           // grid-team barrier words (count, generation)
-  LayerDev L[kMaxLayers];
-  Program prog[N_PROGS];
+  unsigned* bar;           // grid-team barrier counter
+  const int* tables;       // int32 table block (LayerDev::o_*)
+  const double* filt;      // contrast filter coefficients
 };
 
 // Per-launch job description (passed by value).
 struct Job {
   int prog;
   int n_nets;
-  const uint8_t* images;   // (N, C, H, W) bytes, or null for host-staged input
-  const float* lut;        // null: `images` holds float32 (N, C, H, W)
+  const uint8_t* images;   // (N, R, C, H, W) bytes, or null for host-staged input
+  const float* lut;        // null: `images` holds float32 (N, R, C, H, W)
   const int32_t* labels;
   const int32_t* order;    // visit order (null: first + t)
   const double* targets;   // explicit targets (n_classes) for single steps
@@ -237,7 +250,7 @@ __device__ __forceinline__ const float* stage(const float* src, int n, const Tea
 // The current image's input values in the CTA's scratch, read straight from
 // the dataset (bytes through the LUT, or f32), so the first layer does not
 // wait a phase for OP_LOAD_INPUT to publish them.  nullptr if they do not fit.
-__device__ __forceinline__ const float* stage_input(const NetDev& N, const TeamCtx& tm,
+__device__ __forceinline__ const float* stage_input(const NetGeo& N, const NetPtr& R, const TeamCtx& tm,
                                                     int& used) {
   const int n = N.in_cells;
   if (used + n > tm.smem_floats) return nullptr;
@@ -256,7 +269,7 @@ __device__ __forceinline__ const float* stage_input(const NetDev& N, const TeamC
 // it and pass it on to their recorded winner (network.py:253-259: zeroed
 // buffer, `+=`, so the winner holds 0 + v); conv / FC multiply by f'(a)
 // (network.py:222,227-228,260-261).
-__device__ __forceinline__ void emit_delta(const NetDev& N, float* act, int s,
+__device__ __forceinline__ void emit_delta(const NetGeo& N, const NetPtr& R, float* act, int s,
                                            int cell, float v) {
   for (;;) {
     const LayerDev& L = N.L[s];
@@ -285,7 +298,7 @@ __device__ __forceinline__ void emit_delta(const NetDev& N, float* act, int s,
 // ---------------------------------------------------------------------------
 // input and contrast layer
 
-__device__ __forceinline__ void op_load_input(const NetDev& N, const Job& job,
+__device__ __forceinline__ void op_load_input(const NetGeo& N, const NetPtr& R, const Job& job,
                                               const Ctx& ctx, const TeamCtx& tm) {
   if (!job.images) return;
   float* y = ctx.act + N.L[0].y_off;
@@ -302,12 +315,12 @@ __device__ __forceinline__ void op_load_input(const NetDev& N, const Job& job,
 
 // correlate(mode="nearest") per (filter, channel): f64 sum, one rounding.
 // One warp per output cell: lanes split the taps, fixed-order xor reduction.
-__device__ __forceinline__ void op_imgproc(const NetDev& N, const LayerDev& L, float* act,
+__device__ __forceinline__ void op_imgproc(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                            const TeamCtx& tm) {
   __syncthreads();   // scratch reuse
   const LayerDev& I = N.L[0];
   int used = 0;
-  const float* src = stage_input(N, tm, used);
+  const float* src = stage_input(N, R, tm, used);
   if (!src) src = act + I.y_off;   // (never: the builder folds only inputs that fit)
   stage_sync();
   float* out = act + L.y_off;
@@ -326,7 +339,7 @@ __device__ __forceinline__ void op_imgproc(const NetDev& N, const LayerDev& L, f
     const int y = pix / L.w, x = pix % L.w;
     const int f = (o - C) / C, c = (o - C) % C;
     const float* s = src + c * hw;
-    const double* k = L.filt + (int64_t)f * taps;
+    const double* k = (R.filt + L.o_filt) + (int64_t)f * taps;
     double acc = 0.0;
     for (int t = lane; t < taps; t += 32) {
       const int i = t / L.fw, j = t % L.fw;
@@ -375,7 +388,7 @@ __device__ __forceinline__ float conv_cell(float acc, const float* src, const in
 // weights (contiguous in the arena: per dest [blocks..., bias]) and source
 // map offsets are staged in shared memory; the source layer too when it fits.
 template <int KX, int KY>
-__device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, float* act,
+__device__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, float* act,
                                const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
   const int hw = L.h * L.w;
@@ -385,10 +398,10 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   if (q0 >= q1) return;
   const int d0 = q0 / hw, d1 = (q1 - 1) / hw;
   const int kk = L.kx * L.ky;
-  const int k0 = __ldg(L.fwd_off + (d0)), k1 = __ldg(L.fwd_off + (d1 + 1));
-  const float* arena = N.params + L.p_off;
-  const int w0 = __ldg(L.fwd_widx + (k0));                      // first weight of map d0
-  const int n_w = __ldg(L.bias_off + (d1)) + 1 - w0;            // through d1's bias
+  const int k0 = __ldg(TB(L, fwd_off) + (d0)), k1 = __ldg(TB(L, fwd_off) + (d1 + 1));
+  const float* arena = R.params + L.p_off;
+  const int w0 = __ldg(TB(L, fwd_widx) + (k0));                      // first weight of map d0
+  const int n_w = __ldg(TB(L, bias_off) + (d1)) + 1 - w0;            // through d1's bias
   const int n_src = S.cells;
 
   // shared layout: [src offsets (k1-k0 ints)] [weights n_w] [source layer]
@@ -398,7 +411,7 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   const bool w_in_smem = (k1 - k0) + n_w <= tm.smem_floats;
   const bool s_in_smem = w_in_smem && (k1 - k0) + n_w + n_src <= tm.smem_floats;
   const float* src_g = act + S.y_off;
-  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = __ldg(L.fwd_src + (k0 + k)) * (S.h * S.w);
+  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = __ldg(TB(L, fwd_src) + (k0 + k)) * (S.h * S.w);
   if (w_in_smem)
     for (int i = threadIdx.x; i < n_w; i += blockDim.x) cp_async4(ws + i, arena + w0 + i);
   if (s_in_smem)
@@ -414,15 +427,15 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const int d = q / hw, pix = q % hw;
     const int r = pix / L.w, c = pix % L.w;
-    const int kb = __ldg(L.fwd_off + (d)), ke = __ldg(L.fwd_off + (d + 1));
-    const float* w = wbase + (__ldg(L.fwd_widx + (kb)) - w0);
+    const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
+    const float* w = wbase + (__ldg(TB(L, fwd_widx) + (kb)) - w0);
     float acc = w[(ke - kb) * kk];                    // bias slot follows the blocks
     const int rc = (r * L.ty) * S.w + c * L.tx;
     if (offs) {
       acc = conv_cell<KX, KY>(acc, sbase + rc, offs + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
     } else {
       for (int k = kb; k < ke; ++k) {
-        const int so = __ldg(L.fwd_src + (k)) * (S.h * S.w);
+        const int so = __ldg(TB(L, fwd_src) + (k)) * (S.h * S.w);
         acc = conv_cell<KX, KY>(acc, sbase + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
       }
     }
@@ -433,18 +446,18 @@ __device__ void conv_fwd_chunk(const NetDev& N, const LayerDev& L, int flags, fl
   __syncthreads();
 }
 
-__device__ __forceinline__ void op_conv_fwd(const NetDev& N, const LayerDev& L, int flags,
+__device__ __forceinline__ void op_conv_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags,
                                             float* act, const TeamCtx& tm) {
-  if (L.kx == 2 && L.ky == 2) conv_fwd_chunk<2, 2>(N, L, flags, act, tm);
-  else if (L.kx == 3 && L.ky == 3) conv_fwd_chunk<3, 3>(N, L, flags, act, tm);
-  else if (L.kx == 4 && L.ky == 4) conv_fwd_chunk<4, 4>(N, L, flags, act, tm);
-  else if (L.kx == 5 && L.ky == 5) conv_fwd_chunk<5, 5>(N, L, flags, act, tm);
-  else conv_fwd_chunk<0, 0>(N, L, flags, act, tm);
+  if (L.kx == 2 && L.ky == 2) conv_fwd_chunk<2, 2>(N, R, L, flags, act, tm);
+  else if (L.kx == 3 && L.ky == 3) conv_fwd_chunk<3, 3>(N, R, L, flags, act, tm);
+  else if (L.kx == 4 && L.ky == 4) conv_fwd_chunk<4, 4>(N, R, L, flags, act, tm);
+  else if (L.kx == 5 && L.ky == 5) conv_fwd_chunk<5, 5>(N, R, L, flags, act, tm);
+  else conv_fwd_chunk<0, 0>(N, R, L, flags, act, tm);
 }
 
 // max-pool (kernels.py:154-172): strict '>' keeps the first cell in scan order.
 // The argmax is stored as an index into the whole source layer.
-__device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L, float* act,
+__device__ __forceinline__ void op_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                             const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
   const float* src = act + S.y_off;
@@ -484,30 +497,31 @@ __device__ __forceinline__ void op_pool_fwd(const NetDev& N, const LayerDev& L, 
 
 // One conv cell from global weights (used for the truncated cells).
 template <int KX, int KY>
-__device__ __forceinline__ float conv_value_global(const LayerDev& L, const LayerDev& S,
+__device__ __forceinline__ float conv_value_global(const NetPtr& R, const LayerDev& L,
+                                                   const LayerDev& S,
                                                    const float* arena, const float* src,
                                                    int d, int r, int c) {
   const int kk = L.kx * L.ky;
-  const int kb = __ldg(L.fwd_off + (d)), ke = __ldg(L.fwd_off + (d + 1));
-  const float* w = arena + __ldg(L.fwd_widx + (kb));
-  float acc = arena[__ldg(L.bias_off + (d))];
+  const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
+  const float* w = arena + __ldg(TB(L, fwd_widx) + (kb));
+  float acc = arena[__ldg(TB(L, bias_off) + (d))];
   const int rc = (r * L.ty) * S.w + c * L.tx;
   for (int k = kb; k < ke; ++k) {
-    const int so = __ldg(L.fwd_src + (k)) * (S.h * S.w);
+    const int so = __ldg(TB(L, fwd_src) + (k)) * (S.h * S.w);
     acc = conv_cell<KX, KY>(acc, src + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
   }
   return acc;
 }
 
 template <int KX, int KY>
-__device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, bool full,
+__device__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, bool full,
                               float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
   const LayerDev& S = N.L[li - 1];
   const LayerDev& P = N.L[li + 1];
   const int hw = L.h * L.w, shw = S.h * S.w, phw = P.h * P.w, blk = P.px * P.py;
   const int kk = L.kx * L.ky;
-  const float* arena = N.params + L.p_off;
+  const float* arena = R.params + L.p_off;
   float* a = act + L.a_off;
   float* y = act + L.y_off;
   float* dl = act + L.d_off;
@@ -521,12 +535,12 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
   const float* src = src_g;
   if (li == 1) {
     if (sp.b < sp.e) {
-      const float* si = stage_input(N, tm, used);
+      const float* si = stage_input(N, R, tm, used);
       if (si) src = si;
     }
   } else if (sp.b < sp.e && S.cells <= tm.smem_floats / 2) {
     // the whole source layer, unless this CTA's maps connect to fewer cells
-    const int nk_all = __ldg(L.fwd_off + ((sp.e - 1) / phw + 1)) - __ldg(L.fwd_off + (sp.b / phw));
+    const int nk_all = __ldg(TB(L, fwd_off) + ((sp.e - 1) / phw + 1)) - __ldg(TB(L, fwd_off) + (sp.b / phw));
     CK_SUBT(tm, 20);
     if (S.cells <= nk_all * shw) src = stage(src, S.cells, tm, used);
     CK_SUBT(tm, 21);
@@ -546,7 +560,7 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
     bool wst = false, slots = false;
     for (int tries = 0; tries < 24; ++tries) {
       const int d0 = q / phw, d1 = (qe - 1) / phw;
-      const int nk = __ldg(L.fwd_off + (d1 + 1)) - __ldg(L.fwd_off + (d0));
+      const int nk = __ldg(TB(L, fwd_off) + (d1 + 1)) - __ldg(TB(L, fwd_off) + (d0));
       const int nw = nk * kk + d1 + 1 - d0;
       const int base = ((nk + 3) & ~3) + ((nw + 3) & ~3) + (qe - q) * blk;
       if (!whole && base + nk * shw <= avail) { wst = slots = true; break; }
@@ -559,7 +573,7 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
     }
     CK_SUBT(tm, 2);
     const int d0 = q / phw, d1 = (qe - 1) / phw;
-    const int k0 = __ldg(L.fwd_off + (d0)), k1 = __ldg(L.fwd_off + (d1 + 1));
+    const int k0 = __ldg(TB(L, fwd_off) + (d0)), k1 = __ldg(TB(L, fwd_off) + (d1 + 1));
     const int w0 = k0 * kk + d0;
     const int nw = (k1 - k0) * kk + d1 + 1 - d0;
     int* soff = reinterpret_cast<int*>(tm.smem + used);
@@ -571,10 +585,10 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       int u2 = used + ((k1 - k0 + 3) & ~3);
       stage(arena + w0, nw, tm, u2);
       for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x)
-        soff[k] = slots ? k * shw : __ldg(L.fwd_src + (k0 + k)) * shw;
+        soff[k] = slots ? k * shw : __ldg(TB(L, fwd_src) + (k0 + k)) * shw;
       if (slots)
         for (int k = (threadIdx.x >> 5); k < k1 - k0; k += (blockDim.x >> 5)) {
-          const float* from = src_g + __ldg(L.fwd_src + (k0 + k)) * shw;
+          const float* from = src_g + __ldg(TB(L, fwd_src) + (k0 + k)) * shw;
           for (int i = lane_id(); i < shw; i += 32) cp_async4(sslot + k * shw + i, from + i);
         }
     }
@@ -589,12 +603,12 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
       const int c = (pp % P.w) * P.px + t % P.px;
       float acc;
       if (wst) {
-        const int kb = __ldg(L.fwd_off + (d)), ke = __ldg(L.fwd_off + (d + 1));
+        const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
         const float* w = ws + (kb * kk + d - w0);
         acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
                                 soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
       } else {
-        acc = conv_value_global<KX, KY>(L, S, arena, src, d, r, c);
+        acc = conv_value_global<KX, KY>(R, L, S, arena, src, d, r, c);
       }
       const int cell = d * hw + r * L.w + c;
       const float yv = conv_act(acc);
@@ -635,7 +649,7 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
         int r, c;
         if (k < strip) { r = k / (L.w - cw); c = cw + k % (L.w - cw); }
         else { r = rh + (k - strip) / L.w; c = (k - strip) % L.w; }
-        const float acc = conv_value_global<KX, KY>(L, S, arena, whole ? src : src_g, d, r, c);
+        const float acc = conv_value_global<KX, KY>(R, L, S, arena, whole ? src : src_g, d, r, c);
         const int cell = d * hw + r * L.w + c;
         a[cell] = acc;
         y[cell] = conv_act(acc);
@@ -646,13 +660,13 @@ __device__ void conv_pool_fwd(const NetDev& N, const LayerDev& L, int flags, boo
   __syncthreads();
 }
 
-__device__ __forceinline__ void op_conv_pool(const NetDev& N, const LayerDev& L, int flags,
+__device__ __forceinline__ void op_conv_pool(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags,
                                              bool full, float* act, const TeamCtx& tm) {
-  if (L.kx == 2 && L.ky == 2) conv_pool_fwd<2, 2>(N, L, flags, full, act, tm);
-  else if (L.kx == 3 && L.ky == 3) conv_pool_fwd<3, 3>(N, L, flags, full, act, tm);
-  else if (L.kx == 4 && L.ky == 4) conv_pool_fwd<4, 4>(N, L, flags, full, act, tm);
-  else if (L.kx == 5 && L.ky == 5) conv_pool_fwd<5, 5>(N, L, flags, full, act, tm);
-  else conv_pool_fwd<0, 0>(N, L, flags, full, act, tm);
+  if (L.kx == 2 && L.ky == 2) conv_pool_fwd<2, 2>(N, R, L, flags, full, act, tm);
+  else if (L.kx == 3 && L.ky == 3) conv_pool_fwd<3, 3>(N, R, L, flags, full, act, tm);
+  else if (L.kx == 4 && L.ky == 4) conv_pool_fwd<4, 4>(N, R, L, flags, full, act, tm);
+  else if (L.kx == 5 && L.ky == 5) conv_pool_fwd<5, 5>(N, R, L, flags, full, act, tm);
+  else conv_pool_fwd<0, 0>(N, R, L, flags, full, act, tm);
 }
 
 // ---------------------------------------------------------------------------
@@ -683,7 +697,7 @@ __device__ __forceinline__ void fc_cols_preact(const float* x, const float* W, i
   __syncthreads();
 }
 
-__device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, float* act,
+__device__ __forceinline__ void op_fc_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                           const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
   const int n_in = S.cells, n_out = L.cells;
@@ -695,7 +709,7 @@ __device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, fl
   used += 2 * kFcSlices * kFcTile;
   float* out_a = tm.smem + used;
   used += kFcTile;
-  const float* W = N.params + L.p_off;
+  const float* W = R.params + L.p_off;
   const bool wst = used + n_in * kFcTile <= tm.smem_floats;
   float* wt = tm.smem + used;
   for (int tile = tm.rank; tile < n_tiles; tile += tm.size) {
@@ -711,7 +725,7 @@ __device__ __forceinline__ void op_fc_fwd(const NetDev& N, const LayerDev& L, fl
       }
     }
     stage_sync();
-    fc_cols_preact(x, wst ? wt : W + j0, wst ? nc : n_out, N.params + L.b_off + j0, n_in, nc,
+    fc_cols_preact(x, wst ? wt : W + j0, wst ? nc : n_out, R.params + L.b_off + j0, n_in, nc,
                    red, out_a);
     if (threadIdx.x < nc) {
       const float aj = out_a[threadIdx.x];
@@ -735,7 +749,7 @@ __device__ __forceinline__ void op_zero_delta(const LayerDev& L, float* act, con
 
 // Output deltas (backprop.py:22-32) and the sample loss (backprop.py:35-39):
 // run by the first warp of team rank 0; lane 0 ends with ctx.loss.
-__device__ __forceinline__ void op_out_delta(const NetDev& N, const Job& job, Ctx& ctx,
+__device__ __forceinline__ void op_out_delta(const NetGeo& N, const NetPtr& R, const Job& job, Ctx& ctx,
                                              double* scratch) {
   const LayerDev& L = N.L[N.n_layers - 1];
   const int n = L.cells;
@@ -755,14 +769,14 @@ __device__ __forceinline__ void op_out_delta(const NetDev& N, const Job& job, Ct
 // FC backward rows (network.py:213-230), one warp per input row i: the row
 // of W is read once for xgrad_i = sum_j W[i,j] delta_j (f64) and then
 // updated in place with grad_w[i,j] = f32(x_i * delta_j) (or stored).
-__device__ __forceinline__ void fc_bwd_rows(const NetDev& N, const LayerDev& L, int li,
+__device__ __forceinline__ void fc_bwd_rows(const NetGeo& N, const NetPtr& R, const LayerDev& L, int li,
                                            int flags, float eta_f, float* act, const float* x,
                                            const float* dl, const TeamCtx& tm) {
   const LayerDev& S = N.L[li - 1];
-  float* W = N.params + L.p_off;
-  float* b = N.params + L.b_off;
-  float* gW = N.grads + L.p_off;
-  float* gb = N.grads + L.b_off;
+  float* W = R.params + L.p_off;
+  float* b = R.params + L.b_off;
+  float* gW = R.grads + L.p_off;
+  float* gb = R.grads + L.b_off;
   const int n_in = S.cells, n_out = L.cells;
   const bool upd = flags & F_UPDATE;
   const int lane = lane_id();
@@ -782,21 +796,21 @@ __device__ __forceinline__ void fc_bwd_rows(const NetDev& N, const LayerDev& L, 
       if (upd) row[j] = sgd(row[j], eta_f, g);
       else gW[(int64_t)i * n_out + j] = g;
     }
-    if (lane == 0 && S.has_delta) emit_delta(N, act, li - 1, i, (float)acc);
+    if (lane == 0 && S.has_delta) emit_delta(N, R, act, li - 1, i, (float)acc);
   }
 }
 
-__device__ __forceinline__ void op_fc_bwd(const NetDev& N, const LayerDev& L, int flags,
+__device__ __forceinline__ void op_fc_bwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags,
                                           float eta_f, float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
-  fc_bwd_rows(N, L, li, flags, eta_f, act, act + N.L[li - 1].y_off, act + L.d_off, tm);
+  fc_bwd_rows(N, R, L, li, flags, eta_f, act, act + N.L[li - 1].y_off, act + L.d_off, tm);
 }
 
 // The output layer in one phase: every CTA recomputes the output layer's
 // forward (a tiny n_in x n_classes product) and the output deltas in its own
 // shared memory, rank 0 publishes a / y / delta and the loss, then all CTAs
 // run the FC backward rows.  Replaces three barrier-separated phases.
-__device__ __forceinline__ void op_fc_out(const NetDev& N, const LayerDev& L, int flags,
+__device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags,
                                           const Job& job, Ctx& ctx, const TeamCtx& tm,
                                           double* scratch) {
   const int li = &L - N.L;
@@ -804,14 +818,14 @@ __device__ __forceinline__ void op_fc_out(const NetDev& N, const LayerDev& L, in
   float* act = ctx.act;
   int used = 0;
   const float* x = stage(act + S.y_off, S.cells, tm, used);
-  const float* W = stage(N.params + L.p_off, S.cells * L.cells, tm, used, 1 << 14);
+  const float* W = stage(R.params + L.p_off, S.cells * L.cells, tm, used, 1 << 14);
   float* yd = tm.smem + used;                    // [a | y | delta] x n_out
   used += (3 * L.cells + 3) & ~3;
   double* red = reinterpret_cast<double*>(tm.smem + used);
   stage_sync();
   for (int j0 = 0; j0 < L.cells; j0 += 32) {
     const int nc = min(32, L.cells - j0);
-    fc_cols_preact(x, W + j0, L.cells, N.params + L.b_off + j0, S.cells, nc, red, yd + j0);
+    fc_cols_preact(x, W + j0, L.cells, R.params + L.b_off + j0, S.cells, nc, red, yd + j0);
   }
   for (int j = threadIdx.x; j < L.cells; j += blockDim.x) yd[L.cells + j] = fc_act(yd[j]);
   __syncthreads();
@@ -832,7 +846,7 @@ __device__ __forceinline__ void op_fc_out(const NetDev& N, const LayerDev& L, in
     if (lane == 0 && tm.rank == 0) ctx.loss = 0.5 * np_pairwise_sum(scratch, n);
   }
   __syncthreads();
-  fc_bwd_rows(N, L, li, flags, job.eta_f, act, x, yd + 2 * L.cells, tm);
+  fc_bwd_rows(N, R, L, li, flags, job.eta_f, act, x, yd + 2 * L.cells, tm);
   __syncthreads();
 }
 
@@ -848,14 +862,15 @@ __device__ __forceinline__ void op_fc_out(const NetDev& N, const LayerDev& L, in
 // shared memory.  With F_UPDATE (only without F_PULL: the pull reads the old
 // weights) the weights are updated in place.
 template <int KX, int KY>
-__device__ __forceinline__ void wgrad_pair(const LayerDev& L, const LayerDev& S, int p,
+__device__ __forceinline__ void wgrad_pair(const NetPtr& R, const LayerDev& L, const LayerDev& S,
+                                           int p,
                                            const float* dl, const float* ys, float* arena,
                                            float* g, bool upd, float eta_f) {
   const int lane = lane_id();
   const int hw = L.h * L.w;
-  const float* d = dl + __ldg(L.pair_dst + (p)) * hw;
-  const float* s = ys + __ldg(L.fwd_src + (p)) * (S.h * S.w);
-  const int o = __ldg(L.fwd_widx + (p));
+  const float* d = dl + __ldg(TB(L, pair_dst) + (p)) * hw;
+  const float* s = ys + __ldg(TB(L, fwd_src) + (p)) * (S.h * S.w);
+  const int o = __ldg(TB(L, fwd_widx) + (p));
   if constexpr (KX > 0) {
     constexpr int KK = KX * KY;
     double part[KK];
@@ -1001,13 +1016,13 @@ __device__ __forceinline__ void wgrad_sparse(const LayerDev& L, const LayerDev& 
 //                block) the old kernel and d's winners, in chunks of whole
 //                source maps
 // Anything that does not fit is read in place from global memory.
-__device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, float eta_f,
+__device__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, float eta_f,
                                 float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
   const LayerDev& S = N.L[li - 1];
   const LayerDev& P = N.L[li + 1];
-  float* arena = N.params + L.p_off;
-  float* g = N.grads + L.p_off;
+  float* arena = R.params + L.p_off;
+  float* g = R.grads + L.p_off;
   const bool upd = flags & F_UPDATE;
   const int shw = S.h * S.w, phw = P.h * P.w;
   const int kk = L.kx * L.ky;
@@ -1027,8 +1042,8 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
   for (int c0 = ts.b; c0 < p1;) {
     int c1 = p1, da, db, need;
     for (;;) {
-      da = __ldg(L.pair_dst + (c0));
-      db = __ldg(L.pair_dst + (c1 - 1));
+      da = __ldg(TB(L, pair_dst) + (c0));
+      db = __ldg(TB(L, pair_dst) + (c1 - 1));
       need = 2 * (db - da + 1) * phw + (c1 - c0) * shw + 8 +
              (split > 1 ? 2 * (c1 - c0) * split * kk + 4 : 0);
       if (need <= cap || c1 - c0 == 1) break;
@@ -1045,7 +1060,7 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
       wdd = stage(wdd, (db - da + 1) * phw, tm, used);
       slots = tm.smem + used;
       for (int p = c0 + warp; p < c1; p += nwarps) {   // one warp per pair's source map
-        const float* from = ys_g + __ldg(L.fwd_src + (p)) * shw;
+        const float* from = ys_g + __ldg(TB(L, fwd_src) + (p)) * shw;
         float* to = slots + (p - c0) * shw;
         for (int i = lane; i < shw; i += 32) cp_async4(to + i, from + i);
       }
@@ -1061,9 +1076,9 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
     }
     for (int task = warp; task < (c1 - c0) * split; task += nwarps) {
       const int p = c0 + task / split, ch = task % split;
-      const int off = (__ldg(L.pair_dst + (p)) - da) * phw;
-      const float* sp = fits ? slots + (p - c0) * shw : ys_g + __ldg(L.fwd_src + (p)) * shw;
-      wgrad_sparse(L, S, __ldg(L.fwd_widx + (p)), wr + off, wdd + off, sp, ch * phw / split,
+      const int off = (__ldg(TB(L, pair_dst) + (p)) - da) * phw;
+      const float* sp = fits ? slots + (p - c0) * shw : ys_g + __ldg(TB(L, fwd_src) + (p)) * shw;
+      wgrad_sparse(L, S, __ldg(TB(L, fwd_widx) + (p)), wr + off, wdd + off, sp, ch * phw / split,
                    (ch + 1) * phw / split, parts ? parts + task * kk : nullptr, arena, g,
                    upd, eta_f);
     }
@@ -1074,7 +1089,7 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
         const int pi = e / kk, t = e % kk;
         double sum = 0.0;
         for (int ch = 0; ch < split; ++ch) sum += parts[(pi * split + ch) * kk + t];
-        emit_wg(__ldg(L.fwd_widx + (c0 + pi)), t, sum, nullptr, arena, g, upd, eta_f);
+        emit_wg(__ldg(TB(L, fwd_widx) + (c0 + pi)), t, sum, nullptr, arena, g, upd, eta_f);
       }
       __syncthreads();
     }
@@ -1088,7 +1103,7 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
     for (int wq = lane; wq < phw; wq += 32) acc += (double)wd_g[d * phw + wq];
     acc = warp_sum(acc);
     if (lane == 0) {
-      const int o = __ldg(L.bias_off + (d));
+      const int o = __ldg(TB(L, bias_off) + (d));
       if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
       else g[o] = (float)acc;
     }
@@ -1110,10 +1125,10 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
   const int per_map = NS * shw * 2;                 // stream buffers (floats)
   for (int m0 = ms.b; m0 < ms.e;) {
     int m1 = min(ms.e, m0 + max(1, nwarps / NCH));
-    int ka = __ldg(L.bwd_off + (m0)), kb = __ldg(L.bwd_off + (m1));
+    int ka = __ldg(TB(L, bwd_off) + (m0)), kb = __ldg(TB(L, bwd_off) + (m1));
     while (m1 - m0 > 1 && (m1 - m0) * per_map + (kb - ka) * (kk + 2 * phw) > cap) {
       --m1;
-      kb = __ldg(L.bwd_off + (m1));
+      kb = __ldg(TB(L, bwd_off) + (m1));
     }
     const int bufs = (m1 - m0) * per_map;
     const bool fits = bufs + (kb - ka) * (kk + 2 * phw) <= cap;
@@ -1124,9 +1139,9 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
     for (int i = threadIdx.x; i < bufs / 2; i += blockDim.x) buf[i] = 0.0;
     if (fits) {
       for (int k = ka + warp; k < kb; k += nwarps) {   // one warp per backward entry
-        const float* wfrom = arena + __ldg(L.bwd_widx + (k));
+        const float* wfrom = arena + __ldg(TB(L, bwd_widx) + (k));
         for (int i = lane; i < kk; i += 32) cp_async4(wst + (k - ka) * kk + i, wfrom + i);
-        const int d = __ldg(L.bwd_dst + (k));
+        const int d = __ldg(TB(L, bwd_dst) + (k));
         for (int i = lane; i < phw; i += 32) {
           cp_async4(wrs + (k - ka) * phw + i, wrc_g + d * phw + i);
           cp_async4(wds + (k - ka) * phw + i, wd_g + d * phw + i);
@@ -1139,7 +1154,7 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
     const int grp = kk >= 32 ? 0 : lane / kk;
     for (int task = warp; task < (m1 - m0) * NCH; task += nwarps) {
       const int mi = task / NCH, ch = task % NCH;
-      const int k0m = __ldg(L.bwd_off + (m0 + mi)), nkm = __ldg(L.bwd_off + (m0 + mi + 1)) - k0m;
+      const int k0m = __ldg(TB(L, bwd_off) + (m0 + mi)), nkm = __ldg(TB(L, bwd_off) + (m0 + mi + 1)) - k0m;
       const int kc0 = k0m + ch * nkm / NCH, kc1 = k0m + (ch + 1) * nkm / NCH;
       for (int t0 = 0; t0 < kk; t0 += 32) {
         const int t = kk >= 32 ? t0 + lane : lane % kk;
@@ -1155,8 +1170,8 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
             wr = wrs + (k - ka) * phw;
             wdd = wds + (k - ka) * phw;
           } else {
-            const int d = __ldg(L.bwd_dst + (k));
-            wk = arena + __ldg(L.bwd_widx + (k));
+            const int d = __ldg(TB(L, bwd_dst) + (k));
+            wk = arena + __ldg(TB(L, bwd_widx) + (k));
             wr = wrc_g + d * phw;
             wdd = wd_g + d * phw;
           }
@@ -1180,7 +1195,7 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
       const double* b = buf + mi * NS * shw + cell;
       double sum = 0.0;
       for (int st = 0; st < NS; ++st) sum += b[st * shw];
-      emit_delta(N, act, li - 1, (m0 + mi) * shw + cell, (float)sum);
+      emit_delta(N, R, act, li - 1, (m0 + mi) * shw + cell, (float)sum);
     }
     __syncthreads();
     CK_SUBT(tm, 19);
@@ -1188,16 +1203,16 @@ __device__ void conv_bwd_sparse(const NetDev& N, const LayerDev& L, int flags, f
   }
 }
 
-__device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, int flags,
+__device__ __forceinline__ void op_conv_bwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags,
                                             float eta_f, float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
   if (L.pool_above) {
-    conv_bwd_sparse(N, L, flags, eta_f, act, tm);
+    conv_bwd_sparse(N, R, L, flags, eta_f, act, tm);
     return;
   }
   const LayerDev& S = N.L[li - 1];
-  float* arena = N.params + L.p_off;
-  float* g = N.grads + L.p_off;
+  float* arena = R.params + L.p_off;
+  float* g = R.grads + L.p_off;
   const bool upd = flags & F_UPDATE;
   const int hw = L.h * L.w, shw = S.h * S.w;
   const int lane = lane_id();
@@ -1210,11 +1225,11 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
   const Span ts = cta_span(total, tm);
   for (int task = ts.b + (threadIdx.x >> 5); task < ts.e; task += blockDim.x >> 5) {
     if (task < n_w) {
-      if (L.kx == 2 && L.ky == 2) wgrad_pair<2, 2>(L, S, task, dl, ys, arena, g, upd, eta_f);
-      else if (L.kx == 3 && L.ky == 3) wgrad_pair<3, 3>(L, S, task, dl, ys, arena, g, upd, eta_f);
-      else if (L.kx == 4 && L.ky == 4) wgrad_pair<4, 4>(L, S, task, dl, ys, arena, g, upd, eta_f);
-      else if (L.kx == 5 && L.ky == 5) wgrad_pair<5, 5>(L, S, task, dl, ys, arena, g, upd, eta_f);
-      else wgrad_pair<0, 0>(L, S, task, dl, ys, arena, g, upd, eta_f);
+      if (L.kx == 2 && L.ky == 2) wgrad_pair<2, 2>(R, L, S, task, dl, ys, arena, g, upd, eta_f);
+      else if (L.kx == 3 && L.ky == 3) wgrad_pair<3, 3>(R, L, S, task, dl, ys, arena, g, upd, eta_f);
+      else if (L.kx == 4 && L.ky == 4) wgrad_pair<4, 4>(R, L, S, task, dl, ys, arena, g, upd, eta_f);
+      else if (L.kx == 5 && L.ky == 5) wgrad_pair<5, 5>(R, L, S, task, dl, ys, arena, g, upd, eta_f);
+      else wgrad_pair<0, 0>(R, L, S, task, dl, ys, arena, g, upd, eta_f);
     } else {
       const int d = task - n_w;
       const float* dd = dl + d * hw;
@@ -1222,7 +1237,7 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
       for (int i = lane; i < hw; i += 32) acc += (double)dd[i];
       acc = warp_sum(acc);
       if (lane == 0) {
-        const int o = __ldg(L.bias_off + (d));
+        const int o = __ldg(TB(L, bias_off) + (d));
         if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
         else g[o] = (float)acc;
       }
@@ -1243,18 +1258,18 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
       // cell, so four destinations share one loop nest: accumulator q takes
       // the destinations k = kb + q (mod 4), combined in fixed order.
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const int kb = __ldg(L.bwd_off + (s)), k1 = __ldg(L.bwd_off + (s + 1));
+      const int kb = __ldg(TB(L, bwd_off) + (s)), k1 = __ldg(TB(L, bwd_off) + (s + 1));
       const int dw0 = (j - ylo * L.ty) * L.kx + i - xlo * L.tx;   // weight index at (ylo, xlo)
       int k = kb;
       for (; k + 4 <= k1; k += 4) {
-        const float* d0 = dl + __ldg(L.bwd_dst + (k)) * hw + ylo * L.w;
-        const float* d1 = dl + __ldg(L.bwd_dst + (k + 1)) * hw + ylo * L.w;
-        const float* d2 = dl + __ldg(L.bwd_dst + (k + 2)) * hw + ylo * L.w;
-        const float* d3 = dl + __ldg(L.bwd_dst + (k + 3)) * hw + ylo * L.w;
-        const float* w0 = arena + __ldg(L.bwd_widx + (k)) + dw0;
-        const float* w1 = arena + __ldg(L.bwd_widx + (k + 1)) + dw0;
-        const float* w2 = arena + __ldg(L.bwd_widx + (k + 2)) + dw0;
-        const float* w3 = arena + __ldg(L.bwd_widx + (k + 3)) + dw0;
+        const float* d0 = dl + __ldg(TB(L, bwd_dst) + (k)) * hw + ylo * L.w;
+        const float* d1 = dl + __ldg(TB(L, bwd_dst) + (k + 1)) * hw + ylo * L.w;
+        const float* d2 = dl + __ldg(TB(L, bwd_dst) + (k + 2)) * hw + ylo * L.w;
+        const float* d3 = dl + __ldg(TB(L, bwd_dst) + (k + 3)) * hw + ylo * L.w;
+        const float* w0 = arena + __ldg(TB(L, bwd_widx) + (k)) + dw0;
+        const float* w1 = arena + __ldg(TB(L, bwd_widx) + (k + 1)) + dw0;
+        const float* w2 = arena + __ldg(TB(L, bwd_widx) + (k + 2)) + dw0;
+        const float* w3 = arena + __ldg(TB(L, bwd_widx) + (k + 3)) + dw0;
         for (int y = ylo; y <= yhi; ++y) {
           for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx) {
             acc[0] += (double)__fmul_rn(d0[x], w0[wi]);
@@ -1267,8 +1282,8 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
         }
       }
       for (; k < k1; ++k) {
-        const float* d = dl + __ldg(L.bwd_dst + (k)) * hw + ylo * L.w;
-        const float* w = arena + __ldg(L.bwd_widx + (k)) + dw0;
+        const float* d = dl + __ldg(TB(L, bwd_dst) + (k)) * hw + ylo * L.w;
+        const float* w = arena + __ldg(TB(L, bwd_widx) + (k)) + dw0;
         double part = 0.0;
         for (int y = ylo; y <= yhi; ++y, d += L.w, w -= L.ty * L.kx)
           for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx)
@@ -1280,43 +1295,43 @@ __device__ __forceinline__ void op_conv_bwd(const NetDev& N, const LayerDev& L, 
           default: acc[3] += part; break;
         }
       }
-      emit_delta(N, act, li - 1, cell, (float)((acc[0] + acc[1]) + (acc[2] + acc[3])));
+      emit_delta(N, R, act, li - 1, cell, (float)((acc[0] + acc[1]) + (acc[2] + acc[3])));
     }
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ void op_update(const NetDev& N, const LayerDev& L, float eta_f,
+__device__ __forceinline__ void op_update(const NetGeo& N, const NetPtr& R, const LayerDev& L, float eta_f,
                                           const TeamCtx& tm) {
-  float* p = N.params + L.p_off;
-  const float* g = N.grads + L.p_off;
+  float* p = R.params + L.p_off;
+  const float* g = R.grads + L.p_off;
   const Span sp = cta_span(L.n_par, tm);
   for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) p[q] = sgd(p[q], eta_f, g[q]);
 }
 
 // Runs the ops of one phase for this thread's share of the team.  Every
 // thread of every CTA calls this (ops may __syncthreads internally).
-__device__ __forceinline__ void run_phase(const NetDev& N, const Program& P, int ph,
+__device__ __forceinline__ void run_phase(const NetGeo& N, const NetPtr& R, const Program& P, int ph,
                                           const Job& job, Ctx& ctx, const TeamCtx& tm,
                                           double* scratch) {
   for (int o = P.begin[ph]; o < P.begin[ph + 1]; ++o) {
     const Op op = P.ops[o];
     const LayerDev& L = N.L[op.layer];
     switch (op.kind) {
-      case OP_LOAD_INPUT: op_load_input(N, job, ctx, tm); break;
-      case OP_IMGPROC: op_imgproc(N, L, ctx.act, tm); break;
-      case OP_CONV_FWD: op_conv_fwd(N, L, op.flags, ctx.act, tm); break;
-      case OP_CONV_POOL: op_conv_pool(N, L, op.flags, job.full != 0, ctx.act, tm); break;
-      case OP_POOL_FWD: op_pool_fwd(N, L, ctx.act, tm); break;
-      case OP_FC_FWD: op_fc_fwd(N, L, ctx.act, tm); break;
+      case OP_LOAD_INPUT: op_load_input(N, R, job, ctx, tm); break;
+      case OP_IMGPROC: op_imgproc(N, R, L, ctx.act, tm); break;
+      case OP_CONV_FWD: op_conv_fwd(N, R, L, op.flags, ctx.act, tm); break;
+      case OP_CONV_POOL: op_conv_pool(N, R, L, op.flags, job.full != 0, ctx.act, tm); break;
+      case OP_POOL_FWD: op_pool_fwd(N, R, L, ctx.act, tm); break;
+      case OP_FC_FWD: op_fc_fwd(N, R, L, ctx.act, tm); break;
       case OP_ZERO_DELTA: op_zero_delta(L, ctx.act, tm); break;
       case OP_OUT_DELTA:
-        if (tm.rank == 0 && threadIdx.x < 32) op_out_delta(N, job, ctx, scratch);
+        if (tm.rank == 0 && threadIdx.x < 32) op_out_delta(N, R, job, ctx, scratch);
         break;
-      case OP_FC_BWD: op_fc_bwd(N, L, op.flags, job.eta_f, ctx.act, tm); break;
-      case OP_FC_OUT: op_fc_out(N, L, op.flags, job, ctx, tm, scratch); break;
-      case OP_CONV_BWD: op_conv_bwd(N, L, op.flags, job.eta_f, ctx.act, tm); break;
-      case OP_UPDATE: op_update(N, L, job.eta_f, tm); break;
+      case OP_FC_BWD: op_fc_bwd(N, R, L, op.flags, job.eta_f, ctx.act, tm); break;
+      case OP_FC_OUT: op_fc_out(N, R, L, op.flags, job, ctx, tm, scratch); break;
+      case OP_CONV_BWD: op_conv_bwd(N, R, L, op.flags, job.eta_f, ctx.act, tm); break;
+      case OP_UPDATE: op_update(N, R, L, job.eta_f, tm); break;
       default: break;
     }
   }

@@ -24,11 +24,14 @@
 
 namespace ck {
 
-constexpr int kMaxNetsPerLaunch = 64;
+constexpr int kMaxNetsPerLaunch = 32;
 constexpr int kScratchDoubles = 1024;  // output-layer scratch (n_classes <= 1024)
 
-struct NetPtrs {
-  NetDev* p[kMaxNetsPerLaunch];
+// Kernel argument: per net of the launch, its geometry (device copy, read by
+// the generic kernels) and its memory.
+struct NetRefs {
+  const NetGeo* geo[kMaxNetsPerLaunch];
+  NetPtr ptr[kMaxNetsPerLaunch];
 };
 
 // ---------------------------------------------------------------------------
@@ -59,7 +62,7 @@ struct ClusterTeam {
     asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
     return r;
   }
-  __device__ static void sync(const NetDev&, int, unsigned&) {
+  __device__ static void sync(const NetPtr&, int, unsigned&) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -73,12 +76,12 @@ struct ClusterTeam {
 struct GridTeam {
   __device__ static unsigned rank(int ctas) { return blockIdx.x % ctas; }
   __device__ static unsigned index(int ctas) { return blockIdx.x / ctas; }
-  __device__ static void sync(const NetDev& N, int ctas, unsigned& target) {
+  __device__ static void sync(const NetPtr& R, int ctas, unsigned& target) {
     __syncthreads();
     if (threadIdx.x == 0) {
       target += (unsigned)ctas;
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(N.bar) : "memory");
-      while ((int)(ld_acquire(N.bar) - target) < 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(R.bar) : "memory");
+      while ((int)(ld_acquire(R.bar) - target) < 0) {
       }
     }
     __syncthreads();
@@ -87,7 +90,7 @@ struct GridTeam {
 
 // Point the team context at the current image (dataset bytes + LUT, f32
 // dataset, or the host-staged input already in the activation arena).
-__device__ __forceinline__ void set_input(const NetDev& N, const Job& job, const Ctx& ctx,
+__device__ __forceinline__ void set_input(const NetGeo& N, const Job& job, const Ctx& ctx,
                                           TeamCtx& tm) {
   tm.in_u8 = nullptr;
   tm.in_lut = nullptr;
@@ -104,10 +107,10 @@ __device__ __forceinline__ void set_input(const NetDev& N, const Job& job, const
 
 // Copy a net descriptor into shared memory (descriptor reads then never
 // touch L1/L2 inside the image loop).
-__device__ __forceinline__ void load_desc(NetDev* dst, const NetDev* src) {
+__device__ __forceinline__ void load_desc(NetGeo* dst, const NetGeo* src) {
   const int4* s = reinterpret_cast<const int4*>(src);
   int4* d = reinterpret_cast<int4*>(dst);
-  for (int i = threadIdx.x; i < (int)(sizeof(NetDev) / sizeof(int4)); i += blockDim.x) d[i] = s[i];
+  for (int i = threadIdx.x; i < (int)(sizeof(NetGeo) / sizeof(int4)); i += blockDim.x) d[i] = s[i];
   __syncthreads();
 }
 
@@ -120,19 +123,15 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
-constexpr size_t kDescBytes = (sizeof(NetDev) + 15) & ~size_t(15);
+constexpr size_t kDescBytes = (sizeof(NetGeo) + 15) & ~size_t(15);
 constexpr size_t kScratchBytes = kScratchDoubles * sizeof(double);
 constexpr int kTeamStageFloats = 48 * 1024;   // 192 KB staging per CTA
 constexpr int kEvalStageFloats = 12 * 1024;   // 48 KB staging per CTA
 
+// Where this CTA sits: its team (net) and rank.
 template <class Team>
-__global__ void __launch_bounds__(CK_TEAM_THREADS, 1)
-net_team_kernel(NetPtrs nets, Job job, int ctas) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  NetDev& N = *reinterpret_cast<NetDev*>(smem);
-  double* scratch = reinterpret_cast<double*>(smem + kDescBytes);
-
-  unsigned rank, team, tsize;
+__device__ __forceinline__ void team_position(int ctas, unsigned& rank, unsigned& team,
+                                              unsigned& tsize) {
   if constexpr (std::is_same<Team, ClusterTeam>::value) {
     rank = ClusterTeam::rank();
     tsize = ClusterTeam::size();
@@ -142,9 +141,17 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
     tsize = ctas;
     team = GridTeam::index(ctas);
   }
-  if ((int)team >= job.n_nets) return;
-  load_desc(&N, nets.p[team]);
+}
 
+// The per-image loop of one team.  RunPhases(ph-loop body) is either the
+// interpreted program (generic kernel) or a compile-time unrolled one
+// (specialised kernels, ck_specs.cuh); everything else is shared.
+template <class Team, class Phases>
+__device__ __forceinline__ void team_loop(const NetGeo& N, const NetPtr& R, const Job& job,
+                                          int ctas, unsigned rank, unsigned team,
+                                          unsigned tsize, unsigned char* work,
+                                          const Phases& phases) {
+  double* scratch = reinterpret_cast<double*>(work);
   const Program& P = N.prog[job.prog];
   TeamCtx tm;
   tm.ph = 0;
@@ -154,10 +161,10 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
   tm.gsize = tsize * blockDim.x;
   tm.gwarp = tm.gtid >> 5;
   tm.gwarps = tm.gsize >> 5;
-  tm.smem = reinterpret_cast<float*>(smem + kDescBytes + kScratchBytes);
+  tm.smem = reinterpret_cast<float*>(work + kScratchBytes);
   tm.smem_floats = kTeamStageFloats;
   Ctx ctx;
-  ctx.act = N.act;
+  ctx.act = R.act;
   ctx.loss = 0.0;
   double total = 0.0;
   // profile record per image: [start, then per phase: barrier exit (rank 0),
@@ -172,19 +179,17 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
     long long* prof = (job.prof && team == 0 && t < job.prof_images)
                           ? job.prof + t * prof_stride : nullptr;
     if (prof && rank == 0 && threadIdx.x == 0) prof[0] = globaltimer();
-    for (int ph = 0; ph < P.n_phases; ++ph) {
-      tm.ph = ph;
-      CK_SUBT(tm, 0);
-      run_phase(N, P, ph, job, ctx, tm, scratch);
+    auto after_phase = [&](int ph) {
       CK_SUBT(tm, 30);
       if (prof) {
         __syncthreads();
         if (threadIdx.x == 0) prof[1 + ph * (1 + tsize) + 1 + rank] = globaltimer();
       }
-      Team::sync(N, ctas, bar_target);
+      Team::sync(R, ctas, bar_target);
       CK_SUBT(tm, 31);
       if (prof && rank == 0 && threadIdx.x == 0) prof[1 + ph * (1 + tsize)] = globaltimer();
-    }
+    };
+    phases(job, ctx, tm, scratch, after_phase);
     if (rank == 0 && threadIdx.x == 0 && job.prog != PROG_FORWARD && job.prog != PROG_APPLY) {
       total += ctx.loss;
       if (job.losses) job.losses[team * job.n + t] = ctx.loss;
@@ -193,15 +198,45 @@ net_team_kernel(NetPtrs nets, Job job, int ctas) {
   if (rank == 0 && threadIdx.x == 0 && job.loss_total) job.loss_total[team] = total;
 }
 
+// Interpreted phase program (any net, any program).
+struct InterpPhases {
+  const NetGeo& N;
+  const NetPtr& R;
+  template <class After>
+  __device__ __forceinline__ void operator()(const Job& job, Ctx& ctx, TeamCtx& tm,
+                                             double* scratch, After& after) const {
+    const Program& P = N.prog[job.prog];
+    for (int ph = 0; ph < P.n_phases; ++ph) {
+      tm.ph = ph;
+      CK_SUBT(tm, 0);
+      run_phase(N, R, P, ph, job, ctx, tm, scratch);
+      after(ph);
+    }
+  }
+};
+
+template <class Team>
+__global__ void __launch_bounds__(CK_TEAM_THREADS, 1)
+net_team_kernel(NetRefs nets, Job job, int ctas) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  NetGeo& N = *reinterpret_cast<NetGeo*>(smem);
+  unsigned rank, team, tsize;
+  team_position<Team>(ctas, rank, team, tsize);
+  if ((int)team >= job.n_nets) return;
+  load_desc(&N, nets.geo[team]);
+  const NetPtr R = nets.ptr[team];
+  team_loop<Team>(N, R, job, ctas, rank, team, tsize, smem + kDescBytes, InterpPhases{N, R});
+}
+
 // ---------------------------------------------------------------------------
 // batched evaluation: every CTA is its own team with a private act arena and
 // runs PROG_EVAL on images first+blockIdx.x, first+blockIdx.x+gridDim.x, ...
 // Same per-neuron arithmetic as training's forward, so labels are identical.
 
 __global__ void __launch_bounds__(256)
-net_eval_kernel(const NetDev* net, Job job) {
+net_eval_kernel(const NetGeo* net, NetPtr R, Job job) {
   extern __shared__ __align__(16) unsigned char smem[];
-  NetDev& N = *reinterpret_cast<NetDev*>(smem);
+  NetGeo& N = *reinterpret_cast<NetGeo*>(smem);
   load_desc(&N, net);
   const Program& P = N.prog[PROG_EVAL];
   TeamCtx tm;
@@ -222,7 +257,7 @@ net_eval_kernel(const NetDev* net, Job job) {
     ctx.img = job.first + t;
     set_input(N, job, ctx, tm);
     for (int ph = 0; ph < P.n_phases; ++ph) {
-      run_phase(N, P, ph, job, ctx, tm, nullptr);
+      run_phase(N, R, P, ph, job, ctx, tm, nullptr);
       __syncthreads();
     }
     const float* y = ctx.act + O.y_off;
@@ -251,8 +286,9 @@ using namespace ck;
 
 struct ck_net {
   int device = 0;
-  NetDev h;                       // host image of the descriptor (device pointers)
-  NetDev* d_desc = nullptr;
+  NetGeo h;                       // geometry + programs (host image)
+  NetGeo* d_desc = nullptr;       // device copy (read by the generic kernels)
+  NetPtr ptr;                     // device memory of the net
   float* d_params = nullptr;
   float* d_grads = nullptr;
   float* d_act = nullptr;
@@ -307,7 +343,7 @@ struct ProgramBuilder {
 };
 
 // `skip_out`: the output layer's forward is folded into OP_FC_OUT.
-void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero,
+void build_forward(ProgramBuilder& b, const NetGeo& N, bool load, bool zero,
                    bool skip_out = false) {
   const int last = skip_out ? N.n_layers - 1 : N.n_layers;
   // The first layer can read the image itself (stage_input) when it is a
@@ -351,7 +387,7 @@ void build_forward(ProgramBuilder& b, const NetDev& N, bool load, bool zero,
 // Backward walk of network.py:205-262 as phases.  With `update`, each
 // learnable layer is updated as soon as nothing later reads its old weights:
 // FC rows in place, a conv whose pull is done in the following phase.
-void build_backward(ProgramBuilder& b, const NetDev& N, bool update) {
+void build_backward(ProgramBuilder& b, const NetGeo& N, bool update) {
   std::vector<int> pending;
   int k = N.n_layers - 1;
   bool done = false;
@@ -390,7 +426,7 @@ void build_backward(ProgramBuilder& b, const NetDev& N, bool update) {
   b.phase();
 }
 
-void build_programs(NetDev& N, bool* ok) {
+void build_programs(NetGeo& N, bool* ok) {
   {
     ProgramBuilder b(N.prog[PROG_TRAIN]);
     build_forward(b, N, true, true, true);
@@ -461,13 +497,14 @@ int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
   int rc = configure_kernels();
   if (rc) return rc;
   const TeamShape t0 = resolve_team(nets[0], n_nets);
-  NetPtrs ptrs;
+  NetRefs ptrs;
   memset(&ptrs, 0, sizeof(ptrs));
   for (int i = 0; i < n_nets; ++i) {
     const TeamShape ti = resolve_team(nets[i], n_nets);
     if (ti.kind != t0.kind || ti.ctas != t0.ctas || ti.threads != t0.threads)
       return set_error(CK_E_CONFIG, "all nets of one launch need the same team config");
-    ptrs.p[i] = nets[i]->d_desc;
+    ptrs.geo[i] = nets[i]->d_desc;
+    ptrs.ptr[i] = nets[i]->ptr;
   }
   job.n_nets = n_nets;
   const int ctas = t0.ctas;
@@ -519,22 +556,13 @@ int run_single(ck_net* net, Job job) {
   return CK_OK;
 }
 
-}  // namespace
-
-extern "C" {
-
-int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net** out) {
-  CK_CHECK(layers && out, CK_E_CONFIG, "null argument");
-  CK_CHECK(n_layers >= 2 && n_layers <= kMaxLayers, CK_E_CONFIG, "layer count out of range");
-  CK_CHECK(layers[0].kind == CK_LAYER_INPUT, CK_E_CONFIG, "first layer must be the input");
-  CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG,
-           "last layer must be fully connected (output)");
-  CK_CUDA_TRY(cudaSetDevice(device));
-
-  ck_net* net = new ck_net();
-  net->device = device;
-  NetDev& N = net->h;
-  memset(&N, 0, sizeof(NetDev));
+// The whole device description of a net from its resolved layers -- pure
+// host code (no CUDA calls), shared by ck_net_create and the spec generator.
+int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
+                       std::vector<int>& tables, std::vector<double>& filt,
+                       int64_t* n_params) {
+  NetGeo& N = *geo;
+  memset(&N, 0, sizeof(NetGeo));
   N.n_layers = n_layers;
 
   int64_t p_cursor = 0, a_cursor = 0, t_cursor = 0, f_cursor = 0;
@@ -549,7 +577,6 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
     if (D.kind == CK_LAYER_FC) L.h = L.w = 1;
     L.cells = L.maps * L.h * L.w;
     if (L.maps < 1 || L.h < 1 || L.w < 1) {
-      delete net;
       return set_error(CK_E_GEOMETRY, "layer " + std::to_string(k) + ": size below 1");
     }
     if (k > 0) {
@@ -605,14 +632,13 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
     std::string where = "layer " + std::to_string(k) + ": ";
     switch (D.kind) {
       case CK_LAYER_INPUT:
-        if (k != 0) { delete net; return set_error(CK_E_CONFIG, where + "input must be first"); }
+        if (k != 0) { return set_error(CK_E_CONFIG, where + "input must be first"); }
         N.in_cells = L.cells;
         break;
       case CK_LAYER_IMGPROC:
         if (k != 1 || D.n_filters < 1 || !D.filter_coeffs || D.filter_h < 1 || D.filter_w < 1 ||
             D.maps != N.L[0].maps * (1 + D.n_filters) || D.width != N.L[0].w ||
             D.height != N.L[0].h) {
-          delete net;
           return set_error(CK_E_CONFIG, where + "bad image-processing layer");
         }
         L.n_filt = D.n_filters;
@@ -625,12 +651,10 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
         const LayerDev& S = N.L[k - 1];
         if (D.kx < 1 || D.ky < 1 || D.sx < 0 || D.sy < 0 ||
             (L.h - 1) * (D.sy + 1) + D.ky > S.h || (L.w - 1) * (D.sx + 1) + D.kx > S.w) {
-          delete net;
           return set_error(CK_E_GEOMETRY, where + "conv geometry does not fit its input");
         }
         if (!D.fwd_offsets || !D.fwd_srcs || !D.fwd_widx || !D.bias_offset ||
             D.arena_size != D.n_pairs * D.kx * D.ky + D.maps) {
-          delete net;
           return set_error(CK_E_CONFIG, where + "incomplete connection table");
         }
         L.kx = D.kx; L.ky = D.ky; L.tx = D.sx + 1; L.ty = D.sy + 1;
@@ -647,7 +671,6 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
       case CK_LAYER_POOL: {
         const LayerDev& S = N.L[k - 1];
         if (D.px < 1 || D.py < 1 || L.maps != S.maps || L.w != S.w / D.px || L.h != S.h / D.py) {
-          delete net;
           return set_error(CK_E_GEOMETRY, where + "pool geometry does not match its input");
         }
         L.px = D.px; L.py = D.py;
@@ -662,25 +685,22 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
         break;
       }
       default:
-        delete net;
         return set_error(CK_E_CONFIG, where + "unknown layer kind");
     }
   }
   for (int k = 0; k < n_layers; ++k)   // work splits use 32-bit (n * team size) products
     if (N.L[k].cells > (1 << 22) || N.L[k].n_par > (1 << 22)) {
-      delete net;
       return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": more than 4M cells/params");
     }
   N.n_classes = N.L[n_layers - 1].cells;
   if (N.n_classes > kScratchDoubles) {
-    delete net;
     return set_error(CK_E_CONFIG, "too many output classes");
   }
   N.act_size = a_cursor;
-  net->n_params = p_cursor;
+  *n_params = p_cursor;
 
   // host staging of the int32 tables
-  std::vector<int> tables(std::max<int64_t>(t_cursor, 1));
+  tables.assign(std::max<int64_t>(t_cursor, 1), 0);
   for (int k = 0; k < n_layers; ++k) {
     if (layers[k].kind != CK_LAYER_CONV) continue;
     const ck_layer_desc& D = layers[k];
@@ -697,7 +717,6 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
     int* pair_dst = t;
     for (int d = 0; d <= L.maps; ++d) fwd_off[d] = (int)D.fwd_offsets[d];
     if (fwd_off[L.maps] != D.n_pairs) {
-      delete net;
       return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": CSR size mismatch");
     }
     std::vector<int> count(n_src, 0);
@@ -705,7 +724,6 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
       const int64_t s = D.fwd_srcs[p];
       if (s < 0 || s >= n_src || D.fwd_widx[p] < 0 ||
           D.fwd_widx[p] + D.kx * D.ky > D.arena_size) {
-        delete net;
         return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": table entry out of range");
       }
       fwd_src[p] = (int)s;
@@ -720,14 +738,12 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
       for (int p = fwd_off[d]; p < fwd_off[d + 1]; ++p) {
         pair_dst[p] = d;
         if (fwd_widx[p] != cursor) {
-          delete net;
           return set_error(CK_E_CONFIG, "layer " + std::to_string(k) +
                                             ": arena is not tiled like ConnectionTable");
         }
         cursor += D.kx * D.ky;
       }
       if (bias[d] != cursor) {
-        delete net;
         return set_error(CK_E_CONFIG, "layer " + std::to_string(k) + ": bias slot out of place");
       }
       cursor += 1;
@@ -745,19 +761,60 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
         fill[s]++;
       }
   }
-  std::vector<double> filt(std::max<int64_t>(f_cursor, 1));
+  filt.assign(std::max<int64_t>(f_cursor, 1), 0.0);
   for (int k = 0; k < n_layers; ++k)
     if (layers[k].kind == CK_LAYER_IMGPROC)
       memcpy(filt.data() + filt_off[k], layers[k].filter_coeffs,
              sizeof(double) * layers[k].n_filters * layers[k].filter_h * layers[k].filter_w);
 
+  for (int k = 0; k < n_layers; ++k) {   // table / filter offsets (LayerDev::o_*)
+    LayerDev& L = N.L[k];
+    if (L.kind == L_CONV) {
+      int t = (int)tab_off[k];
+      const int n_src = N.L[k - 1].maps;
+      L.o_fwd_off = t;   t += L.maps + 1;
+      L.o_fwd_src = t;   t += L.n_pairs;
+      L.o_fwd_widx = t;  t += L.n_pairs;
+      L.o_bias_off = t;  t += L.maps;
+      L.o_bwd_off = t;   t += n_src + 1;
+      L.o_bwd_dst = t;   t += L.n_pairs;
+      L.o_bwd_widx = t;  t += L.n_pairs;
+      L.o_pair_dst = t;
+    }
+    if (L.kind == L_IMGPROC) L.o_filt = (int)filt_off[k];
+  }
   bool ok = true;
   build_programs(N, &ok);
-  if (!ok) {
-    delete net;
-    return set_error(CK_E_CONFIG, "network too deep for the phase program");
-  }
+  if (!ok) return set_error(CK_E_CONFIG, "network too deep for the phase program");
+  return CK_OK;
 
+}
+
+}  // namespace
+
+extern "C" {
+
+int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net** out) {
+  CK_CHECK(layers && out, CK_E_CONFIG, "null argument");
+  CK_CHECK(n_layers >= 2 && n_layers <= kMaxLayers, CK_E_CONFIG, "layer count out of range");
+  CK_CHECK(layers[0].kind == CK_LAYER_INPUT, CK_E_CONFIG, "first layer must be the input");
+  CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG,
+           "last layer must be fully connected (output)");
+  CK_CUDA_TRY(cudaSetDevice(device));
+
+  ck_net* net = new ck_net();
+  net->device = device;
+  std::vector<int> tables;
+  std::vector<double> filt;
+  {
+    const int rc = build_net_geometry(layers, n_layers, &net->h, tables, filt, &net->n_params);
+    if (rc) {
+      delete net;
+      return rc;
+    }
+  }
+  NetGeo& N = net->h;
+  const int64_t p_cursor = net->n_params;
   auto fail = [&](int rc) {
     ck_net_destroy(net);
     return rc;
@@ -766,7 +823,7 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
 #define CK_ALLOC(ptr, bytes)                                        \
   e = cudaMalloc((void**)&(ptr), (bytes));                          \
   if (e != cudaSuccess) return fail(cuda_status(e, "cudaMalloc"));
-  CK_ALLOC(net->d_desc, sizeof(NetDev));
+  CK_ALLOC(net->d_desc, sizeof(NetGeo));
   CK_ALLOC(net->d_params, sizeof(float) * std::max<int64_t>(p_cursor, 1));
   CK_ALLOC(net->d_grads, sizeof(float) * std::max<int64_t>(p_cursor, 1));
   CK_ALLOC(net->d_act, sizeof(float) * N.act_size);
@@ -779,31 +836,17 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
   e = cudaStreamCreateWithFlags(&net->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) return fail(cuda_status(e, "cudaStreamCreate"));
 
-  N.params = net->d_params;
-  N.grads = net->d_grads;
-  N.act = net->d_act;
-  N.bar = net->d_bar;
-  for (int k = 0; k < n_layers; ++k) {
-    LayerDev& L = N.L[k];
-    if (L.kind == L_CONV) {
-      int* t = net->d_tables + tab_off[k];
-      const int n_src = N.L[k - 1].maps;
-      L.fwd_off = t;   t += L.maps + 1;
-      L.fwd_src = t;   t += L.n_pairs;
-      L.fwd_widx = t;  t += L.n_pairs;
-      L.bias_off = t;  t += L.maps;
-      L.bwd_off = t;   t += n_src + 1;
-      L.bwd_dst = t;   t += L.n_pairs;
-      L.bwd_widx = t;  t += L.n_pairs;
-      L.pair_dst = t;
-    }
-    if (L.kind == L_IMGPROC) L.filt = net->d_filters + filt_off[k];
-  }
+  net->ptr.params = net->d_params;
+  net->ptr.grads = net->d_grads;
+  net->ptr.act = net->d_act;
+  net->ptr.bar = net->d_bar;
+  net->ptr.tables = net->d_tables;
+  net->ptr.filt = net->d_filters;
   e = cudaMemcpy(net->d_tables, tables.data(), sizeof(int) * tables.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return fail(cuda_status(e, "upload tables"));
   e = cudaMemcpy(net->d_filters, filt.data(), sizeof(double) * filt.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return fail(cuda_status(e, "upload filters"));
-  e = cudaMemcpy(net->d_desc, &N, sizeof(NetDev), cudaMemcpyHostToDevice);
+  e = cudaMemcpy(net->d_desc, &N, sizeof(NetGeo), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return fail(cuda_status(e, "upload descriptor"));
   e = cudaMemset(net->d_bar, 0, 2 * sizeof(unsigned));
   if (e != cudaSuccess) return fail(cuda_status(e, "zero barrier"));
@@ -1167,7 +1210,8 @@ int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut, int64_t fi
   job.pred = pred;
   job.outputs = outputs;
   job.eval_scratch = net->d_eval;
-  net_eval_kernel<<<ctas, 256, eval_smem_bytes(), (cudaStream_t)stream>>>(net->d_desc, job);
+  net_eval_kernel<<<ctas, 256, eval_smem_bytes(), (cudaStream_t)stream>>>(net->d_desc, net->ptr,
+                                                                          job);
   count_launch();
   CK_CUDA_TRY(cudaGetLastError());
   return CK_OK;
