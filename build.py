@@ -18,7 +18,7 @@ PKG = os.path.join(ROOT, "paper_1102_0183_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libckb200.so")
 SOURCES = ["ck_seam.cu", "ck_net.cu"]
-HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_host.h"]
+HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_host.h", "ck_specs.inc"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -42,14 +42,39 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+SPECS = os.path.join(CSRC, "ck_specs.inc")
+
+
+def _compile(out: str, verbose: bool, extra=()) -> None:
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+
+
+def generate_specs(lib: str) -> bool:
+    """Regenerate ck_specs.inc with `lib`'s geometry builder; True if changed."""
+    before = open(SPECS).read() if os.path.exists(SPECS) else None
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_specs.py"), lib, SPECS],
+                   check=True)
+    return open(SPECS).read() != before
+
+
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
+    """Two stages: a library without specialised kernels (its geometry builder
+    prints ck_specs.inc for the BASELINE nets), then the full library."""
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "ckb200.h"))
+    deps.append(os.path.join(ROOT, "paper_1102_0183_b200", "configs.py"))
+    deps.remove(SPECS)
     if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES]]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.run(cmd, check=True)
+        # stage 1: the library without specialised kernels generates the specs
+        stage1 = os.path.join(PKG, "libckb200_stage1.so")
+        _compile(stage1, False, ["-DCK_NO_SPECS"])
+        generate_specs(stage1)
+        os.remove(stage1)
+        # stage 2: the library with them
+        _compile(LIB, verbose)
     return LIB
 
 

@@ -209,6 +209,19 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
  * 4 eval) for diagnostics and DESIGN.md. */
 int ck_net_describe_program(const ck_net* net, int prog, char* buf, int cap);
 
+/* Specialised training kernels.  Nets whose geometry equals one compiled
+ * into the library (the BASELINE configs, generated from
+ * paper_1102_0183_b200/configs.py) train with a kernel in which every size,
+ * offset and op choice is a compile-time constant; results are bit-identical
+ * to the generic kernel.  ck_net_spec_source prints the C++ spec of a net
+ * (host only, used by the build); ck_net_set_specialized(net, 0) forces the
+ * generic kernel; ck_net_kernel_info names the kernel a training launch uses
+ * ("specialised:<name>" or "generic"). */
+int ck_net_spec_source(const ck_layer_desc* layers, int n_layers, const char* name, char* buf,
+                       int64_t cap, int64_t* len);
+int ck_net_set_specialized(ck_net* net, int enable);
+int ck_net_kernel_info(const ck_net* net, char* buf, int cap);
+
 /* Development aid: arm per-phase sub-timers of the training kernel.  Thread
  * 0 of team rank `rank` writes %globaltimer at numbered points into
  * dev_buf[phase * 32 + point] (>= 32 * n_phases int64, device); NULL disarms. */

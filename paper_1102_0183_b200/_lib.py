@@ -85,6 +85,10 @@ _SIGNATURES = {
                                     C.POINTER(_i32)]),
     "ck_net_describe_program": (_i32, [_vp, _i32, C.c_char_p, _i32]),
     "ck_debug_subprof": (_i32, [_vp, _i32]),
+    "ck_net_spec_source": (_i32, [C.POINTER(LayerDesc), _i32, C.c_char_p, C.c_char_p, _i64,
+                                  C.POINTER(_i64)]),
+    "ck_net_set_specialized": (_i32, [_vp, _i32]),
+    "ck_net_kernel_info": (_i32, [_vp, C.c_char_p, _i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

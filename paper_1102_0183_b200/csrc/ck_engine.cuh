@@ -269,9 +269,13 @@ __device__ __forceinline__ const float* stage_input(const NetGeo& N, const NetPt
 // it and pass it on to their recorded winner (network.py:253-259: zeroed
 // buffer, `+=`, so the winner holds 0 + v); conv / FC multiply by f'(a)
 // (network.py:222,227-228,260-261).
+// At most kMaxPoolChain pools in a row (an unrolled walk keeps every layer
+// index a compile-time constant in the specialised kernels).
+constexpr int kMaxPoolChain = 4;
 __device__ __forceinline__ void emit_delta(const NetGeo& N, const NetPtr& R, float* act, int s,
                                            int cell, float v) {
-  for (;;) {
+#pragma unroll
+  for (int hop = 0; hop <= kMaxPoolChain; ++hop) {
     const LayerDev& L = N.L[s];
     if (L.kind == L_POOL) {
       act[L.d_off + cell] = v;
@@ -388,7 +392,7 @@ __device__ __forceinline__ float conv_cell(float acc, const float* src, const in
 // weights (contiguous in the arena: per dest [blocks..., bias]) and source
 // map offsets are staged in shared memory; the source layer too when it fits.
 template <int KX, int KY>
-__device__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, float* act,
+__device__ __forceinline__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, float* act,
                                const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
   const int hw = L.h * L.w;
@@ -514,7 +518,7 @@ __device__ __forceinline__ float conv_value_global(const NetPtr& R, const LayerD
 }
 
 template <int KX, int KY>
-__device__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, bool full,
+__device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, bool full,
                               float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
   const LayerDev& S = N.L[li - 1];
@@ -1016,7 +1020,7 @@ __device__ __forceinline__ void wgrad_sparse(const LayerDev& L, const LayerDev& 
 //                block) the old kernel and d's winners, in chunks of whole
 //                source maps
 // Anything that does not fit is read in place from global memory.
-__device__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, float eta_f,
+__device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, float eta_f,
                                 float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
   const LayerDev& S = N.L[li - 1];
@@ -1309,32 +1313,35 @@ __device__ __forceinline__ void op_update(const NetGeo& N, const NetPtr& R, cons
   for (int q = sp.b + threadIdx.x; q < sp.e; q += blockDim.x) p[q] = sgd(p[q], eta_f, g[q]);
 }
 
+__device__ __forceinline__ void run_op(const NetGeo& N, const NetPtr& R, const Op op,
+                                       const Job& job, Ctx& ctx, const TeamCtx& tm,
+                                       double* scratch) {
+  const LayerDev& L = N.L[op.layer];
+  switch (op.kind) {
+    case OP_LOAD_INPUT: op_load_input(N, R, job, ctx, tm); break;
+    case OP_IMGPROC: op_imgproc(N, R, L, ctx.act, tm); break;
+    case OP_CONV_FWD: op_conv_fwd(N, R, L, op.flags, ctx.act, tm); break;
+    case OP_CONV_POOL: op_conv_pool(N, R, L, op.flags, job.full != 0, ctx.act, tm); break;
+    case OP_POOL_FWD: op_pool_fwd(N, R, L, ctx.act, tm); break;
+    case OP_FC_FWD: op_fc_fwd(N, R, L, ctx.act, tm); break;
+    case OP_ZERO_DELTA: op_zero_delta(L, ctx.act, tm); break;
+    case OP_OUT_DELTA:
+      if (tm.rank == 0 && threadIdx.x < 32) op_out_delta(N, R, job, ctx, scratch);
+      break;
+    case OP_FC_BWD: op_fc_bwd(N, R, L, op.flags, job.eta_f, ctx.act, tm); break;
+    case OP_FC_OUT: op_fc_out(N, R, L, op.flags, job, ctx, tm, scratch); break;
+    case OP_CONV_BWD: op_conv_bwd(N, R, L, op.flags, job.eta_f, ctx.act, tm); break;
+    case OP_UPDATE: op_update(N, R, L, job.eta_f, tm); break;
+    default: break;
+  }
+}
+
 // Runs the ops of one phase for this thread's share of the team.  Every
 // thread of every CTA calls this (ops may __syncthreads internally).
 __device__ __forceinline__ void run_phase(const NetGeo& N, const NetPtr& R, const Program& P, int ph,
                                           const Job& job, Ctx& ctx, const TeamCtx& tm,
                                           double* scratch) {
-  for (int o = P.begin[ph]; o < P.begin[ph + 1]; ++o) {
-    const Op op = P.ops[o];
-    const LayerDev& L = N.L[op.layer];
-    switch (op.kind) {
-      case OP_LOAD_INPUT: op_load_input(N, R, job, ctx, tm); break;
-      case OP_IMGPROC: op_imgproc(N, R, L, ctx.act, tm); break;
-      case OP_CONV_FWD: op_conv_fwd(N, R, L, op.flags, ctx.act, tm); break;
-      case OP_CONV_POOL: op_conv_pool(N, R, L, op.flags, job.full != 0, ctx.act, tm); break;
-      case OP_POOL_FWD: op_pool_fwd(N, R, L, ctx.act, tm); break;
-      case OP_FC_FWD: op_fc_fwd(N, R, L, ctx.act, tm); break;
-      case OP_ZERO_DELTA: op_zero_delta(L, ctx.act, tm); break;
-      case OP_OUT_DELTA:
-        if (tm.rank == 0 && threadIdx.x < 32) op_out_delta(N, R, job, ctx, scratch);
-        break;
-      case OP_FC_BWD: op_fc_bwd(N, R, L, op.flags, job.eta_f, ctx.act, tm); break;
-      case OP_FC_OUT: op_fc_out(N, R, L, op.flags, job, ctx, tm, scratch); break;
-      case OP_CONV_BWD: op_conv_bwd(N, R, L, op.flags, job.eta_f, ctx.act, tm); break;
-      case OP_UPDATE: op_update(N, R, L, job.eta_f, tm); break;
-      default: break;
-    }
-  }
+  for (int o = P.begin[ph]; o < P.begin[ph + 1]; ++o) run_op(N, R, P.ops[o], job, ctx, tm, scratch);
 }
 
 }  // namespace ck

@@ -9,6 +9,7 @@
 // delta, backward with in-place updates) separated by team barriers.
 #include <cooperative_groups.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -17,6 +18,11 @@
 
 #include "ck_engine.cuh"
 #include "ck_host.h"
+#ifndef CK_NO_SPECS
+#include "ck_specs.inc"   // generated: the specialised nets (tools/gen_specs.py)
+#else
+#define CK_SPEC_LIST(X)   // stage-1 build (the generator's own library)
+#endif
 
 #ifndef CK_TEAM_THREADS
 #define CK_TEAM_THREADS 512
@@ -149,10 +155,9 @@ __device__ __forceinline__ void team_position(int ctas, unsigned& rank, unsigned
 template <class Team, class Phases>
 __device__ __forceinline__ void team_loop(const NetGeo& N, const NetPtr& R, const Job& job,
                                           int ctas, unsigned rank, unsigned team,
-                                          unsigned tsize, unsigned char* work,
+                                          unsigned tsize, unsigned char* work, int n_phases,
                                           const Phases& phases) {
   double* scratch = reinterpret_cast<double*>(work);
-  const Program& P = N.prog[job.prog];
   TeamCtx tm;
   tm.ph = 0;
   tm.rank = rank;
@@ -169,7 +174,7 @@ __device__ __forceinline__ void team_loop(const NetGeo& N, const NetPtr& R, cons
   double total = 0.0;
   // profile record per image: [start, then per phase: barrier exit (rank 0),
   // work end of every CTA (after its last warp)] -- globaltimer ns
-  const int prof_stride = 1 + P.n_phases * (1 + (int)tsize);
+  const int prof_stride = 1 + n_phases * (1 + (int)tsize);
   unsigned bar_target = 0;
   for (int64_t t = 0; t < job.n; ++t) {
     ctx.t = t;
@@ -225,7 +230,67 @@ net_team_kernel(NetRefs nets, Job job, int ctas) {
   if ((int)team >= job.n_nets) return;
   load_desc(&N, nets.geo[team]);
   const NetPtr R = nets.ptr[team];
-  team_loop<Team>(N, R, job, ctas, rank, team, tsize, smem + kDescBytes, InterpPhases{N, R});
+  team_loop<Team>(N, R, job, ctas, rank, team, tsize, smem + kDescBytes,
+                  N.prog[job.prog].n_phases, InterpPhases{N, R});
+}
+
+// ---------------------------------------------------------------------------
+// Specialised training kernels.  ck_specs.inc (generated by
+// tools/gen_specs.py from configs.ARCH through ck_net_spec_source) holds one
+// struct per BASELINE net whose constexpr geo() is the exact NetGeo that
+// build_net_geometry produces for it.  The kernel below walks PROG_TRAIN's
+// phases and ops by compile-time recursion, so every layer index, size,
+// offset and op choice is a constant: no interpreter, no runtime division,
+// only the code the net needs.  Same ops, same arithmetic as the generic
+// kernel -- results are bit-identical (tests/test_gpu_parity.py).
+
+template <class Spec, int PH, int O>
+struct SpecOps {
+  __device__ static __forceinline__ void run(const NetPtr& R, const Job& job, Ctx& ctx,
+                                             const TeamCtx& tm, double* scratch) {
+    if constexpr (O < Spec::geo().prog[PROG_TRAIN].begin[PH + 1]) {
+      constexpr Op op = Spec::geo().prog[PROG_TRAIN].ops[O];
+      run_op(Spec::dev(), R, op, job, ctx, tm, scratch);
+      SpecOps<Spec, PH, O + 1>::run(R, job, ctx, tm, scratch);
+    }
+  }
+};
+
+template <class Spec, int PH>
+struct SpecPhase {
+  template <class After>
+  __device__ static __forceinline__ void run(const NetPtr& R, const Job& job, Ctx& ctx,
+                                             TeamCtx& tm, double* scratch, After& after) {
+    if constexpr (PH < Spec::geo().prog[PROG_TRAIN].n_phases) {
+      tm.ph = PH;
+      CK_SUBT(tm, 0);
+      SpecOps<Spec, PH, Spec::geo().prog[PROG_TRAIN].begin[PH]>::run(R, job, ctx, tm, scratch);
+      after(PH);
+      SpecPhase<Spec, PH + 1>::run(R, job, ctx, tm, scratch, after);
+    }
+  }
+};
+
+template <class Spec>
+struct SpecPhases {
+  const NetPtr& R;
+  template <class After>
+  __device__ __forceinline__ void operator()(const Job& job, Ctx& ctx, TeamCtx& tm,
+                                             double* scratch, After& after) const {
+    SpecPhase<Spec, 0>::run(R, job, ctx, tm, scratch, after);
+  }
+};
+
+template <class Spec, class Team>
+__global__ void __launch_bounds__(CK_TEAM_THREADS, 1)
+net_spec_kernel(NetRefs nets, Job job, int ctas) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned rank, team, tsize;
+  team_position<Team>(ctas, rank, team, tsize);
+  if ((int)team >= job.n_nets) return;
+  const NetPtr R = nets.ptr[team];
+  team_loop<Team>(Spec::dev(), R, job, ctas, rank, team, tsize, smem + kDescBytes,
+                  Spec::geo().prog[PROG_TRAIN].n_phases, SpecPhases<Spec>{R});
 }
 
 // ---------------------------------------------------------------------------
@@ -289,6 +354,8 @@ struct ck_net {
   NetGeo h;                       // geometry + programs (host image)
   NetGeo* d_desc = nullptr;       // device copy (read by the generic kernels)
   NetPtr ptr;                     // device memory of the net
+  int spec = -1;                  // index in spec_table() (-1: generic kernel only)
+  int use_spec = 1;               // ck_net_set_specialized
   float* d_params = nullptr;
   float* d_grads = nullptr;
   float* d_act = nullptr;
@@ -477,6 +544,30 @@ int configure_kernels() {
   return CK_OK;
 }
 
+struct SpecEntry {
+  const char* name;
+  NetGeo geo;
+  const void* kernel;   // net_spec_kernel<Spec, GridTeam>
+};
+
+#define CK_SPEC_ENTRY(S) {#S, S::geo(), reinterpret_cast<const void*>(net_spec_kernel<S, GridTeam>)},
+const SpecEntry* spec_table(int* n) {
+  static const SpecEntry table[] = {CK_SPEC_LIST(CK_SPEC_ENTRY){nullptr, NetGeo{}, nullptr}};
+  *n = (int)(sizeof(table) / sizeof(table[0])) - 1;
+  return table;
+}
+#undef CK_SPEC_ENTRY
+
+int configure_spec_kernel(const void* kernel) {
+  static std::vector<const void*> done;
+  for (const void* k : done)
+    if (k == kernel) return CK_OK;
+  CK_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)team_smem_bytes()));
+  done.push_back(kernel);
+  return CK_OK;
+}
+
 // The team a launch of n_nets nets uses.  AUTO = a cooperative grid team
 // spanning the whole GPU: one 512-thread CTA per SM, the SMs shared evenly
 // between the nets of a committee (measured faster than 16-CTA clusters on
@@ -518,6 +609,19 @@ int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
+  // the specialised kernel when every net of the launch has the same spec
+  const void* spec_kernel = nullptr;
+  if (t0.kind == CK_TEAM_GRID && job.prog == PROG_TRAIN && nets[0]->spec >= 0) {
+    bool same = true;
+    for (int i = 0; i < n_nets; ++i)
+      same = same && nets[i]->spec == nets[0]->spec && nets[i]->use_spec;
+    if (same) {
+      int n_spec = 0;
+      spec_kernel = spec_table(&n_spec)[nets[0]->spec].kernel;
+      rc = configure_spec_kernel(spec_kernel);
+      if (rc) return rc;
+    }
+  }
   if (t0.kind == CK_TEAM_GRID) {
     for (int i = 0; i < n_nets; ++i) {   // arrival counters start at 0 every launch
       e = cudaMemsetAsync(nets[i]->d_bar, 0, 2 * sizeof(unsigned), st);
@@ -525,7 +629,12 @@ int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
     }
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
-    e = cudaLaunchKernelEx(&cfg, net_team_kernel<GridTeam>, ptrs, job, ctas);
+    if (spec_kernel) {
+      void* args[] = {&ptrs, &job, (void*)&ctas};
+      e = cudaLaunchKernelExC(&cfg, spec_kernel, args);
+    } else {
+      e = cudaLaunchKernelEx(&cfg, net_team_kernel<GridTeam>, ptrs, job, ctas);
+    }
   } else {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = ctas;
@@ -790,6 +899,87 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
 
 }
 
+// ---- specialised kernels: registry, geometry matching, source printer
+
+bool layer_equal(const LayerDev& a, const LayerDev& b) {
+#define CK_EQ(t, f) if (a.f != b.f) return false;
+  CK_LAYER_FIELDS(CK_EQ)
+#undef CK_EQ
+  return true;
+}
+
+bool geo_equal(const NetGeo& a, const NetGeo& b) {
+  if (a.n_layers != b.n_layers || a.n_classes != b.n_classes || a.in_cells != b.in_cells ||
+      a.act_size != b.act_size)
+    return false;
+  for (int k = 0; k < a.n_layers; ++k)
+    if (!layer_equal(a.L[k], b.L[k])) return false;
+  for (int p = 0; p < N_PROGS; ++p) {
+    const Program& x = a.prog[p];
+    const Program& y = b.prog[p];
+    if (x.n_phases != y.n_phases) return false;
+    for (int i = 0; i <= x.n_phases; ++i)
+      if (x.begin[i] != y.begin[i]) return false;
+    for (int o = 0; o < x.begin[x.n_phases]; ++o)
+      if (x.ops[o].kind != y.ops[o].kind || x.ops[o].layer != y.ops[o].layer ||
+          x.ops[o].flags != y.ops[o].flags)
+        return false;
+  }
+  return true;
+}
+
+int find_spec(const NetGeo& g) {
+  int n = 0;
+  const SpecEntry* t = spec_table(&n);
+  for (int i = 0; i < n; ++i)
+    if (geo_equal(g, t[i].geo)) return i;
+  return -1;
+}
+
+// C++ source of `struct <name>` whose constexpr geo() equals g.
+std::string spec_source(const NetGeo& g, const char* name) {
+  std::string o;
+  char b[256];
+  o += "struct " + std::string(name) + " {\n";
+  o += "  __host__ __device__ static constexpr NetGeo geo() {\n    NetGeo g{};\n";
+  snprintf(b, sizeof b, "    g.n_layers = %d; g.n_classes = %d; g.in_cells = %d; g.act_size = %lldLL;\n",
+           g.n_layers, g.n_classes, g.in_cells, (long long)g.act_size);
+  o += b;
+  for (int k = 0; k < g.n_layers; ++k) {
+    const LayerDev& L = g.L[k];
+    o += "    g.L[" + std::to_string(k) + "] = LayerDev{";
+    bool first = true;
+#define CK_PR(t, f)                                            \
+  o += first ? "" : ", ";                                       \
+  first = false;                                                \
+  o += std::to_string((long long)L.f) + (sizeof(t) == 8 ? "LL" : "");
+    CK_LAYER_FIELDS(CK_PR)
+#undef CK_PR
+    o += "};\n";
+  }
+  for (int p = 0; p < N_PROGS; ++p) {
+    const Program& P = g.prog[p];
+    snprintf(b, sizeof b, "    g.prog[%d].n_phases = %d;\n", p, P.n_phases);
+    o += b;
+    for (int i = 0; i <= P.n_phases; ++i) {
+      snprintf(b, sizeof b, "    g.prog[%d].begin[%d] = %d;\n", p, i, P.begin[i]);
+      o += b;
+    }
+    for (int i = 0; i < P.begin[P.n_phases]; ++i) {
+      snprintf(b, sizeof b, "    g.prog[%d].ops[%d] = Op{%d, %d, %d, 0};\n", p, i, P.ops[i].kind,
+               P.ops[i].layer, P.ops[i].flags);
+      o += b;
+    }
+  }
+  o += "    return g;\n  }\n";
+  o += "  __device__ static const NetGeo& dev();\n};\n";
+  // an immutable device object: loads from it fold to immediates
+  o += "__device__ constexpr NetGeo kGeo_" + std::string(name) + " = " + name + "::geo();\n";
+  o += "__device__ inline const NetGeo& " + std::string(name) + "::dev() { return kGeo_" + name +
+       "; }\n";
+  return o;
+}
+
 }  // namespace
 
 extern "C" {
@@ -815,6 +1005,8 @@ int ck_net_create(const ck_layer_desc* layers, int n_layers, int device, ck_net*
   }
   NetGeo& N = net->h;
   const int64_t p_cursor = net->n_params;
+  net->spec = find_spec(N);
+  if (getenv("CKB200_NO_SPEC")) net->use_spec = 0;   // A/B switch for measurements
   auto fail = [&](int rc) {
     ck_net_destroy(net);
     return rc;
@@ -1148,6 +1340,43 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
     phase_ns[p] = work / n;
     phase_ns[np + p] = bar / n;
   }
+  return CK_OK;
+}
+
+int ck_net_spec_source(const ck_layer_desc* layers, int n_layers, const char* name, char* buf,
+                       int64_t cap, int64_t* len) {
+  CK_CHECK(layers && name && len, CK_E_CONFIG, "null argument");
+  CK_CHECK(n_layers >= 2 && n_layers <= kMaxLayers, CK_E_CONFIG, "layer count out of range");
+  NetGeo* g = new NetGeo();
+  std::vector<int> tables;
+  std::vector<double> filt;
+  int64_t n_params = 0;
+  const int rc = build_net_geometry(layers, n_layers, g, tables, filt, &n_params);
+  if (rc) {
+    delete g;
+    return rc;
+  }
+  const std::string src = spec_source(*g, name);
+  delete g;
+  *len = (int64_t)src.size();
+  if (buf && cap > (int64_t)src.size()) memcpy(buf, src.c_str(), src.size() + 1);
+  return CK_OK;
+}
+
+int ck_net_set_specialized(ck_net* net, int enable) {
+  CK_CHECK(net, CK_E_CONFIG, "null net");
+  net->use_spec = enable ? 1 : 0;
+  return CK_OK;
+}
+
+int ck_net_kernel_info(const ck_net* net, char* buf, int cap) {
+  CK_CHECK(net && buf && cap > 0, CK_E_CONFIG, "null argument");
+  int n = 0;
+  const SpecEntry* t = spec_table(&n);
+  if (net->spec >= 0 && net->use_spec)
+    snprintf(buf, cap, "specialised:%s", t[net->spec].name);
+  else
+    snprintf(buf, cap, "generic");
   return CK_OK;
 }
 

@@ -48,28 +48,58 @@ __device__ __forceinline__ int ceil_div_clamp0(int n, int t) {
 
 // numpy pairwise summation of a contiguous f64 vector (the `.sum()` in
 // backprop.sample_loss): sequential below 8 elements, 8 partial sums up to
-// 128, recursive halving above.
-__device__ inline double np_pairwise_sum(const double* v, int n) {
+// 128, recursive halving above (n2 = n/2 rounded down to a multiple of 8).
+__device__ __forceinline__ double np_pairwise_block(const double* v, int n) {
   if (n < 8) {
     double res = 0.0;
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, v[i]);
     return res;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = v[j];
-    int i = 8;
-    const int full = n - (n % 8);
-    for (; i < full; i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, v[i]);
-    return res;
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = v[j];
+  int i = 8;
+  const int full = n - (n % 8);
+  for (; i < full; i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], v[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, v[i]);
+  return res;
+}
+
+// The halving recursion unrolled with an explicit stack (no device recursion):
+// leaves (<= 128 elements) are summed left to right and combined bottom-up
+// exactly as numpy's recursion combines them.
+__device__ inline double np_pairwise_sum(const double* v, int n) {
+  if (n <= 128) return np_pairwise_block(v, n);
+  // post-order walk: stack of (offset, length, partial sum state)
+  int off[16], len[16], state[16];
+  double left[16];
+  int sp = 0;
+  off[0] = 0; len[0] = n; state[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    const int o = off[sp], m = len[sp];
+    if (m <= 128) {
+      ret = np_pairwise_block(v + o, m);
+      --sp;
+      continue;
+    }
+    int n2 = m / 2;
+    n2 -= n2 % 8;
+    if (state[sp] == 0) {            // descend left
+      state[sp] = 1;
+      ++sp; off[sp] = o; len[sp] = n2; state[sp] = 0;
+    } else if (state[sp] == 1) {     // left done: descend right
+      left[sp] = ret;
+      state[sp] = 2;
+      ++sp; off[sp] = o + n2; len[sp] = m - n2; state[sp] = 0;
+    } else {                         // both done
+      ret = __dadd_rn(left[sp], ret);
+      --sp;
+    }
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise_sum(v, n2), np_pairwise_sum(v + n2, n - n2));
+  return ret;
 }
 
 }  // namespace ck

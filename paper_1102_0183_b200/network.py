@@ -97,6 +97,57 @@ class LayerView:
         return self._net._read_buffer(self.index, BUF_GRAD, np.float32, (n,))
 
 
+def layer_descs(spec: NetworkSpec, table_seed: int = DEFAULT_TABLE_SEED):
+    """The C-ABI description of a resolved net: (ck_layer_desc array, host
+    arrays it points into, connection tables, parameter layout, parameter
+    count).  Tables are the reference's: seeded ``[table_seed, layer_idx]``
+    random tables (network.py:103-108) or full tables."""
+    descs = (_lib.LayerDesc * len(spec.layers))()
+    keep = []                            # host arrays alive while descs are used
+    tables: dict[int, ConnectionTable] = {}
+    layout: list[tuple[int, str, tuple, int]] = []
+    offset = 0
+    for idx, ls in enumerate(spec.layers):
+        prev = spec.layers[idx - 1] if idx else None
+        d = descs[idx]
+        d.kind = KIND_CODES[ls.kind]
+        d.maps, d.width, d.height = ls.out_maps, ls.out_width, ls.out_height
+        if ls.kind == "image_processing":
+            bank, fh, fw = _padded_bank(ls.filters)
+            keep.append(bank)
+            d.n_filters, d.filter_h, d.filter_w = bank.shape[0], fh, fw
+            d.filter_coeffs = bank.ctypes.data
+        elif ls.kind == "convolutional":
+            if ls.connectivity == "random":
+                table = build_random_table(prev.out_maps, ls.maps, ls.in_degree,
+                                           [table_seed, idx], ls.kernel)
+            else:
+                table = build_full_table(prev.out_maps, ls.maps, ls.kernel)
+            tables[idx] = table
+            d.kx, d.ky = table.kx, table.ky
+            d.sx, d.sy = ls.skip
+            d.n_pairs = table.n_pairs
+            d.arena_size = table.arena_size
+            arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in
+                      (table._fwd_offsets, table._fwd_srcs, table._fwd_widx,
+                       table.bias_offset)]
+            keep.extend(arrays)
+            d.fwd_offsets, d.fwd_srcs, d.fwd_widx, d.bias_offset = (
+                a.ctypes.data for a in arrays)
+            layout.append((idx, "arena", (table.arena_size,), offset))
+            offset += table.arena_size
+        elif ls.kind == "max_pooling":
+            d.px, d.py = ls.pool
+        elif ls.kind in ("fully_connected", "output"):
+            n_in = (prev.out_maps * prev.out_width * prev.out_height
+                    if prev.is_spatial else prev.neurons)
+            layout.append((idx, "weights", (n_in, ls.neurons), offset))
+            offset += n_in * ls.neurons
+            layout.append((idx, "bias", (ls.neurons,), offset))
+            offset += ls.neurons
+    return descs, keep, tables, layout, offset
+
+
 class NetworkState:
     """All weights plus device scratch state for one network instance."""
 
@@ -117,58 +168,18 @@ class NetworkState:
         self.tables: dict[int, ConnectionTable] = {}
         self._param_layout: list[tuple[int, str, tuple, int]] = []
 
-        descs = (_lib.LayerDesc * len(spec.layers))()
-        keep = []                            # host arrays alive during create
+        descs, keep, self.tables, self._param_layout, self._n_params = layer_descs(
+            spec, table_seed)
         self.layers: list[LayerView] = []
-        offset = 0
         for idx, ls in enumerate(spec.layers):
-            prev = spec.layers[idx - 1] if idx else None
-            d = descs[idx]
-            d.kind = KIND_CODES[ls.kind]
-            d.maps, d.width, d.height = ls.out_maps, ls.out_width, ls.out_height
-            table = None
-            if ls.kind == "image_processing":
-                bank, fh, fw = _padded_bank(ls.filters)
-                keep.append(bank)
-                d.n_filters, d.filter_h, d.filter_w = bank.shape[0], fh, fw
-                d.filter_coeffs = bank.ctypes.data
-            elif ls.kind == "convolutional":
-                if ls.connectivity == "random":
-                    table = build_random_table(prev.out_maps, ls.maps, ls.in_degree,
-                                               [table_seed, idx], ls.kernel)
-                else:
-                    table = build_full_table(prev.out_maps, ls.maps, ls.kernel)
-                self.tables[idx] = table
-                d.kx, d.ky = table.kx, table.ky
-                d.sx, d.sy = ls.skip
-                d.n_pairs = table.n_pairs
-                d.arena_size = table.arena_size
-                arrays = [np.ascontiguousarray(a, dtype=np.int64) for a in
-                          (table._fwd_offsets, table._fwd_srcs, table._fwd_widx,
-                           table.bias_offset)]
-                keep.extend(arrays)
-                d.fwd_offsets, d.fwd_srcs, d.fwd_widx, d.bias_offset = (
-                    a.ctypes.data for a in arrays)
-                self._param_layout.append((idx, "arena", (table.arena_size,), offset))
-                offset += table.arena_size
-            elif ls.kind == "max_pooling":
-                d.px, d.py = ls.pool
-            elif ls.kind in ("fully_connected", "output"):
-                n_in = (prev.out_maps * prev.out_width * prev.out_height
-                        if prev.is_spatial else prev.neurons)
-                self._param_layout.append((idx, "weights", (n_in, ls.neurons), offset))
-                offset += n_in * ls.neurons
-                self._param_layout.append((idx, "bias", (ls.neurons,), offset))
-                offset += ls.neurons
             if ls.is_spatial:
                 shape = (ls.out_maps, ls.out_height, ls.out_width)
             else:
                 shape = (ls.neurons,)
-            self.layers.append(LayerView(self, idx, ls.kind, shape, table,
+            self.layers.append(LayerView(self, idx, ls.kind, shape, self.tables.get(idx),
                                          ls.pool if ls.kind == "max_pooling" else None,
                                          ls.skip if ls.kind == "convolutional" else None,
                                          ls.filters or None))
-        self._n_params = offset
 
         handle = C.c_void_p()
         _lib.call("ck_net_create", descs, len(spec.layers), device, C.byref(handle))
@@ -208,6 +219,16 @@ class NetworkState:
         k, c, t = C.c_int(), C.c_int(), C.c_int()
         _lib.call("ck_net_get_team", self.handle, C.byref(k), C.byref(c), C.byref(t))
         return k.value, c.value, t.value
+
+    def kernel_info(self) -> str:
+        """Training kernel of this net: "specialised:<spec>" or "generic"."""
+        buf = C.create_string_buffer(256)
+        _lib.call("ck_net_kernel_info", self.handle, buf, len(buf))
+        return buf.value.decode()
+
+    def set_specialized(self, enable: bool) -> None:
+        """Allow (default) or forbid the net's specialised training kernel."""
+        _lib.call("ck_net_set_specialized", self.handle, 1 if enable else 0)
 
     def describe_program(self, prog: int = 0) -> str:
         """Phase program of the engine (0 train, 1 forward, 2 backward,

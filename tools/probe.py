@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--imgs", type=int, default=2000)
     ap.add_argument("--configs", default="C1,C2,C3,C4")
     ap.add_argument("--teams", default="1,16,512;1,8,512;2,148,512;2,74,512")
+    ap.add_argument("--generic", action="store_true", help="force the generic kernel")
     args = ap.parse_args()
     for name in args.configs.split(","):
         with warnings.catch_warnings():
@@ -58,15 +59,19 @@ def main():
         for team in teams:
             try:
                 net = ck.NetworkState(spec, 0, team=team)
+                if args.generic:
+                    net.set_specialized(False)
                 ck.train_epoch(net, data.limit(50), cfg, 0)
                 ms = timed(lambda: ck.train_epoch(net, data, cfg, 0))
-                print(f"{name} train team={team}: {ms:.2f} ms / {n} imgs -> "
+                print(f"{name} [{net.kernel_info()}] train team={team}: {ms:.2f} ms / {n} imgs -> "
                       f"{n / ms * 1e3:.0f} img/s ({ms / n * 1e3:.2f} us/img)", flush=True)
                 net.close()
             except Exception as exc:  # keep probing other shapes
                 print(f"{name} team={team} failed: {exc}", flush=True)
         for team in ((1, 16, 512), (2, 148, 512)):
             net = ck.NetworkState(spec, 0, team=team)
+            if args.generic:
+                net.set_specialized(False)
             if team[0] == 1:
                 print(net.describe_program(0), flush=True)
             work, bar = ck.training.profile_phases(net, data.limit(200))
