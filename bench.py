@@ -416,7 +416,7 @@ def run_ours(args):
             "e2e": e2e,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "net_team_kernel (persistent online-training kernel)",
+                         "kernel": f"persistent online-training kernel ({net.kernel_info()})",
                          "peak_basis": f"FP32 SIMT: {props.multi_processor_count} SMs x "
                                        f"{FP32_LANES_PER_SM} lanes x 2 FLOP x {sm_max:.0f} MHz "
                                        "(not in MEASURED_PEAKS.json)"},

@@ -10,22 +10,25 @@
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_1102_0183_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libckb200.so")
 SOURCES = ["ck_seam.cu", "ck_net.cu"]
-HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_host.h", "ck_specs.inc"]
+HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_kernels.cuh", "ck_host.h", "ck_specs.inc"]
 
-NVCC_FLAGS = [
+COMPILE_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-I", os.path.join(ROOT, "include"),
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared"]
 
 
 def _nvcc() -> str:
@@ -45,15 +48,33 @@ def _stale(target: str, deps: list[str]) -> bool:
 SPECS = os.path.join(CSRC, "ck_specs.inc")
 
 
-def _compile(out: str, verbose: bool, extra=()) -> None:
-    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.run(cmd, check=True)
+def _spec_units() -> list[str]:
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.startswith("ck_spec_") and f.endswith(".cu"))
+
+
+def _compile(out: str, verbose: bool, extra=(), specs: bool = True) -> None:
+    """Every translation unit to an object in parallel, then one link."""
+    units = [os.path.join(CSRC, s) for s in SOURCES] + (_spec_units() if specs else [])
+    tmp = tempfile.mkdtemp(prefix="ckb200_build_")
+    try:
+        procs = []
+        for u in units:
+            obj = os.path.join(tmp, os.path.basename(u) + ".o")
+            cmd = [_nvcc(), *COMPILE_FLAGS, *extra, "-c", "-o", obj, u]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            procs.append((obj, subprocess.Popen(cmd)))
+        for obj, p in procs:
+            if p.wait() != 0:
+                raise subprocess.CalledProcessError(p.returncode, "nvcc")
+        subprocess.run([_nvcc(), *LINK_FLAGS, "-o", out, *[o for o, _ in procs]], check=True)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
 
 
 def generate_specs(lib: str) -> bool:
-    """Regenerate ck_specs.inc with `lib`'s geometry builder; True if changed."""
+    """Regenerate ck_specs.inc (+ ck_spec_*.cu) with `lib`'s geometry builder."""
     before = open(SPECS).read() if os.path.exists(SPECS) else None
     subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_specs.py"), lib, SPECS],
                    check=True)
@@ -62,7 +83,8 @@ def generate_specs(lib: str) -> bool:
 
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     """Two stages: a library without specialised kernels (its geometry builder
-    prints ck_specs.inc for the BASELINE nets), then the full library."""
+    prints ck_specs.inc and one ck_spec_<net>.cu per BASELINE net), then the
+    full library."""
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(ROOT, "include", "ckb200.h"))
     deps.append(os.path.join(ROOT, "paper_1102_0183_b200", "configs.py"))
@@ -70,7 +92,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     if force or _stale(LIB, deps):
         # stage 1: the library without specialised kernels generates the specs
         stage1 = os.path.join(PKG, "libckb200_stage1.so")
-        _compile(stage1, False, ["-DCK_NO_SPECS"])
+        _compile(stage1, False, ["-DCK_NO_SPECS"], specs=False)
         generate_specs(stage1)
         os.remove(stage1)
         # stage 2: the library with them

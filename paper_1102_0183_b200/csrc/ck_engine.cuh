@@ -86,7 +86,7 @@ enum OpKind {
   OP_CONV_POOL,       // conv a, y fused with the max-pool above it (y, argmax)
 };
 
-enum OpFlags { F_UPDATE = 1, F_PULL = 2, F_ZERO_SELF = 4 };
+enum OpFlags { F_UPDATE = 1, F_PULL = 2, F_ZERO_SELF = 4, F_FUSE_BELOW = 8 };
 
 struct Op {
   int16_t kind;
@@ -145,6 +145,8 @@ struct Job {
   float* eval_scratch;     // eval: per-CTA act arenas
   long long* prof;         // phase end times (globaltimer ns), nullable
   int64_t prof_images;     // images profiled
+  long long* sub;          // sub-phase timers (ck_debug_subprof), nullable
+  int sub_rank;
   int full;                // 1: also compute values nothing downstream reads (conv
                            // cells a pool truncates, dense conv deltas) for readback
 };
@@ -160,6 +162,8 @@ struct Ctx {
 // Where this thread sits in its team, plus the CTA's shared scratch.
 struct TeamCtx {
   int ph;                  // current phase (sub-phase timers)
+  long long* sub;          // sub-phase timer buffer (nullptr: off)
+  int sub_rank;
   int rank, size;          // CTA rank in the team / CTAs in the team
   int gtid, gsize;         // thread index / count over the team
   int gwarp, gwarps;       // warp index / count over the team
@@ -174,16 +178,14 @@ struct TeamCtx {
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Development timers (ck_debug_subprof): when armed, thread 0 of team rank
-// c_sub_rank records %globaltimer at numbered points of every phase into
-// c_sub[phase * 32 + point] (last image wins).  Unarmed cost: one constant load.
-__constant__ long long* c_sub;
-__constant__ int c_sub_rank;
+// tm.sub_rank records %globaltimer at numbered points of every phase into
+// tm.sub[phase * 32 + point] (last image wins).  Unarmed cost: one test.
 #define CK_SUBT(tm, i)                                                        \
   do {                                                                        \
-    if (c_sub && threadIdx.x == 0 && (tm).rank == c_sub_rank) {               \
+    if ((tm).sub && threadIdx.x == 0 && (tm).rank == (tm).sub_rank) {         \
       long long _t;                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                  \
-      c_sub[(tm).ph * 32 + (i)] = _t;                                         \
+      (tm).sub[(tm).ph * 32 + (i)] = _t;                                      \
     }                                                                         \
   } while (0)
 
@@ -383,6 +385,59 @@ __device__ __forceinline__ float conv_cell(float acc, const float* src, const in
       const float* wk = w + k * kk;
       for (int v = 0; v < ky; ++v)
         for (int u = 0; u < kx; ++u) acc = __fadd_rn(acc, __fmul_rn(wk[v * kx + u], s[v * sw + u]));
+    }
+  }
+  return acc;
+}
+
+// conv_cell for operands that are all in shared memory (the staged path):
+// explicit ld.shared (no generic-address loads), and the raw operands of
+// source k+1 are loaded before source k's add chain runs, so the chain --
+// bias, then k, v, u in order, every product and sum rounded separately, as
+// kernels.py:78-86 -- is not stalled on load latency.  Bit-identical to
+// conv_cell.
+__device__ __forceinline__ float lds_f32(unsigned addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int lds_s32(unsigned addr) {
+  int v;
+  asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+template <int KX, int KY>
+__device__ __forceinline__ float conv_cell_smem(float acc, const float* src, const int* soff,
+                                                const float* w, int nk, int sw) {
+  constexpr int KK = KX * KY;
+  const unsigned s0 = (unsigned)__cvta_generic_to_shared(src);
+  const unsigned o0 = (unsigned)__cvta_generic_to_shared(soff);
+  const unsigned w0 = (unsigned)__cvta_generic_to_shared(w);
+  float xc[KK], wc[KK];
+  {
+    const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0);
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      xc[t] = lds_f32(sb + 4u * ((t / KX) * sw + t % KX));
+      wc[t] = lds_f32(w0 + 4u * t);
+    }
+  }
+  for (int k = 0; k < nk; ++k) {
+    float xn[KK], wn[KK];
+    const int kn = k + 1 < nk ? k + 1 : k;
+    const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0 + 4u * kn);
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      xn[t] = lds_f32(sb + 4u * ((t / KX) * sw + t % KX));
+      wn[t] = lds_f32(w0 + 4u * (kn * KK + t));
+    }
+#pragma unroll
+    for (int t = 0; t < KK; ++t) acc = __fadd_rn(acc, __fmul_rn(wc[t], xc[t]));
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      xc[t] = xn[t];
+      wc[t] = wn[t];
     }
   }
   return acc;
@@ -609,8 +664,17 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
       if (wst) {
         const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
         const float* w = ws + (kb * kk + d - w0);
-        acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
-                                soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+        if constexpr (KX > 0) {
+          if (whole || slots)   // weights, offsets and sources all in shared memory
+            acc = conv_cell_smem<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
+                                         soff + (kb - k0), w, ke - kb, S.w);
+          else
+            acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
+                                    soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+        } else {
+          acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
+                                  soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+        }
       } else {
         acc = conv_value_global<KX, KY>(R, L, S, arena, src, d, r, c);
       }
@@ -775,7 +839,8 @@ __device__ __forceinline__ void op_out_delta(const NetGeo& N, const NetPtr& R, c
 // updated in place with grad_w[i,j] = f32(x_i * delta_j) (or stored).
 __device__ __forceinline__ void fc_bwd_rows(const NetGeo& N, const NetPtr& R, const LayerDev& L, int li,
                                            int flags, float eta_f, float* act, const float* x,
-                                           const float* dl, const TeamCtx& tm) {
+                                           const float* dl, const TeamCtx& tm,
+                                           bool emit = true) {
   const LayerDev& S = N.L[li - 1];
   float* W = R.params + L.p_off;
   float* b = R.params + L.b_off;
@@ -800,7 +865,7 @@ __device__ __forceinline__ void fc_bwd_rows(const NetGeo& N, const NetPtr& R, co
       if (upd) row[j] = sgd(row[j], eta_f, g);
       else gW[(int64_t)i * n_out + j] = g;
     }
-    if (lane == 0 && S.has_delta) emit_delta(N, R, act, li - 1, i, (float)acc);
+    if (emit && lane == 0 && S.has_delta) emit_delta(N, R, act, li - 1, i, (float)acc);
   }
 }
 
@@ -823,8 +888,8 @@ __device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, cons
   int used = 0;
   const float* x = stage(act + S.y_off, S.cells, tm, used);
   const float* W = stage(R.params + L.p_off, S.cells * L.cells, tm, used, 1 << 14);
-  float* yd = tm.smem + used;                    // [a | y | delta] x n_out
-  used += (3 * L.cells + 3) & ~3;
+  float* yd = tm.smem + used;                    // [a | y | delta] x n_out (+ H's deltas)
+  used += (3 * L.cells + ((flags & F_FUSE_BELOW) ? S.cells : 0) + 3) & ~3;
   double* red = reinterpret_cast<double*>(tm.smem + used);
   stage_sync();
   for (int j0 = 0; j0 < L.cells; j0 += 32) {
@@ -850,7 +915,38 @@ __device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, cons
     if (lane == 0 && tm.rank == 0) ctx.loss = 0.5 * np_pairwise_sum(scratch, n);
   }
   __syncthreads();
-  fc_bwd_rows(N, R, L, li, flags, job.eta_f, act, x, yd + 2 * L.cells, tm);
+  if (!(flags & F_FUSE_BELOW)) {
+    fc_bwd_rows(N, R, L, li, flags, job.eta_f, act, x, yd + 2 * L.cells, tm);
+    __syncthreads();
+    return;
+  }
+  // F_FUSE_BELOW: the FC layer below (H) in the same phase.  Every CTA
+  // derives ALL of H's deltas itself -- one warp per row of this layer's W,
+  // the same f64 fma chain + xor tree as fc_bwd_rows, so the values equal
+  // the unfused ones -- then runs its share of H's backward rows.  This
+  // layer's own gradients are stored (its update waits for the next phase:
+  // every CTA read its weights above).
+  const LayerDev& H = S;
+  float* dh = yd + 3 * L.cells;                  // H's deltas, all rows
+  {
+    const int lane = lane_id(), n_out = L.cells;
+    const float* dl = yd + 2 * n_out;
+    for (int i = threadIdx.x >> 5; i < H.cells; i += blockDim.x >> 5) {
+      const float* row = W + i * n_out;
+      double acc = 0.0;
+      for (int j = lane; j < n_out; j += 32) acc = fma((double)row[j], (double)dl[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) dh[i] = (float)acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < H.cells; i += blockDim.x) {   // f'(a) in parallel
+      dh[i] = __fmul_rn(dh[i], act_deriv(act[H.a_off + i]));
+      if (tm.rank == 0) act[H.d_off + i] = dh[i];
+    }
+  }
+  __syncthreads();
+  fc_bwd_rows(N, R, L, li, 0, job.eta_f, act, x, yd + 2 * L.cells, tm, false);
+  fc_bwd_rows(N, R, H, li - 1, flags & F_UPDATE, job.eta_f, act, act + N.L[li - 2].y_off, dh, tm);
   __syncthreads();
 }
 

@@ -24,9 +24,10 @@ __device__ __forceinline__ float conv_act(float a) {
 }
 
 // numpy's float32 tanh is a SIMD approximation (~1 ulp from correctly
-// rounded in a third of the cases); the device uses the correctly rounded
-// value of the f64 tanh.  Stated tolerance: <= 2 ulp on FC activations.
-__device__ __forceinline__ float tanh32(float z) { return (float)tanh((double)z); }
+// rounded in a third of the cases); the device uses CUDA's tanhf (<= 2 ulp).
+// Stated tolerance: a few ulp on FC activations and on every delta (the conv
+// activation, which must be bit-exact, keeps the reference's f64 tanh).
+__device__ __forceinline__ float tanh32(float z) { return tanhf(z); }
 
 __device__ __forceinline__ float fc_act(float a) {
   return __fmul_rn((float)kActScale, tanh32(__fmul_rn((float)kActGain, a)));
