@@ -47,7 +47,7 @@ enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
   X(int, kx) X(int, ky) X(int, tx) X(int, ty) X(int, px) X(int, py)          \
   X(int, n_pairs) X(int, has_delta) X(int, n_filt) X(int, fh) X(int, fw)     \
   X(int, max_fan_in) X(int, pool_above) X(int, wg_winner_major)              \
-  X(int, wg_split) X(int, pull_g) X(int, pull_ch)                            \
+  X(int, wg_split) X(int, pull_g) X(int, pull_ch) X(int, full)               \
   X(int64_t, p_off) X(int64_t, b_off) X(int64_t, n_par)                      \
   X(int64_t, y_off) X(int64_t, a_off) X(int64_t, d_off) X(int64_t, arg_off)  \
   X(int64_t, wrc_off) X(int64_t, wd_off)                                     \
@@ -57,7 +57,9 @@ enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
 
 // Field notes: tx = sx + 1 (conv stride); pool_above: the next layer is a
 // max-pool (sparse backward); wg_*: weight-gradient lane layout / winner
-// chunks; pull_g / pull_ch: pull lane groups / backward-list chunks;
+// chunks; pull_g / pull_ch: pull lane groups / backward-list chunks; full:
+// the conv table is the full table in ConnectionTable's order, so every table
+// entry is arithmetic (no loads);
 // *_off: act-arena offsets (elements); wrc_off / wd_off: a pool over a conv
 // keeps winner (r<<16|c) and winner delta per pooled cell; o_*: offsets of
 // the conv tables (int32, read-only for a launch, always read with __ldg)
@@ -70,6 +72,8 @@ struct LayerDev {
 
 // table access: TB(L, fwd_off) -> const int* into the table block
 #define TB(L, f) (R.tables + (L).o_##f)
+
+
 
 enum OpKind {
   OP_LOAD_INPUT = 0,  // input y <- lut[image bytes] (no-op for host-staged x)
@@ -125,6 +129,37 @@ struct NetPtr {
   const int* tables;       // int32 table block (LayerDev::o_*)
   const double* filt;      // contrast filter coefficients
 };
+
+// Table entries.  A full table (L.full) in ConnectionTable's order (dest
+// major, sources ascending; arena per dest = its blocks then its bias,
+// topology.py:82-116) is pure arithmetic; otherwise the entry is loaded.
+__device__ __forceinline__ int t_fwd_off(const NetPtr& R, const LayerDev& L, int d) {
+  return L.full ? d * L.src_maps : __ldg(TB(L, fwd_off) + d);
+}
+__device__ __forceinline__ int t_fwd_src(const NetPtr& R, const LayerDev& L, int p) {
+  return L.full ? p % L.src_maps : __ldg(TB(L, fwd_src) + p);
+}
+__device__ __forceinline__ int t_fwd_widx(const NetPtr& R, const LayerDev& L, int p) {
+  return L.full ? (p / L.src_maps) * (L.src_maps * L.kx * L.ky + 1) + (p % L.src_maps) * L.kx * L.ky
+                : __ldg(TB(L, fwd_widx) + p);
+}
+__device__ __forceinline__ int t_bias_off(const NetPtr& R, const LayerDev& L, int d) {
+  return L.full ? d * (L.src_maps * L.kx * L.ky + 1) + L.src_maps * L.kx * L.ky
+                : __ldg(TB(L, bias_off) + d);
+}
+__device__ __forceinline__ int t_pair_dst(const NetPtr& R, const LayerDev& L, int p) {
+  return L.full ? p / L.src_maps : __ldg(TB(L, pair_dst) + p);
+}
+__device__ __forceinline__ int t_bwd_off(const NetPtr& R, const LayerDev& L, int s) {
+  return L.full ? s * L.maps : __ldg(TB(L, bwd_off) + s);
+}
+__device__ __forceinline__ int t_bwd_dst(const NetPtr& R, const LayerDev& L, int k) {
+  return L.full ? k % L.maps : __ldg(TB(L, bwd_dst) + k);
+}
+__device__ __forceinline__ int t_bwd_widx(const NetPtr& R, const LayerDev& L, int k) {
+  return L.full ? (k % L.maps) * (L.src_maps * L.kx * L.ky + 1) + (k / L.maps) * L.kx * L.ky
+                : __ldg(TB(L, bwd_widx) + k);
+}
 
 // Per-launch job description (passed by value).
 struct Job {
@@ -457,10 +492,10 @@ __device__ __forceinline__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R,
   if (q0 >= q1) return;
   const int d0 = q0 / hw, d1 = (q1 - 1) / hw;
   const int kk = L.kx * L.ky;
-  const int k0 = __ldg(TB(L, fwd_off) + (d0)), k1 = __ldg(TB(L, fwd_off) + (d1 + 1));
+  const int k0 = t_fwd_off(R, L, (d0)), k1 = t_fwd_off(R, L, (d1 + 1));
   const float* arena = R.params + L.p_off;
-  const int w0 = __ldg(TB(L, fwd_widx) + (k0));                      // first weight of map d0
-  const int n_w = __ldg(TB(L, bias_off) + (d1)) + 1 - w0;            // through d1's bias
+  const int w0 = t_fwd_widx(R, L, (k0));                      // first weight of map d0
+  const int n_w = t_bias_off(R, L, (d1)) + 1 - w0;            // through d1's bias
   const int n_src = S.cells;
 
   // shared layout: [src offsets (k1-k0 ints)] [weights n_w] [source layer]
@@ -470,7 +505,7 @@ __device__ __forceinline__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R,
   const bool w_in_smem = (k1 - k0) + n_w <= tm.smem_floats;
   const bool s_in_smem = w_in_smem && (k1 - k0) + n_w + n_src <= tm.smem_floats;
   const float* src_g = act + S.y_off;
-  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = __ldg(TB(L, fwd_src) + (k0 + k)) * (S.h * S.w);
+  for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = t_fwd_src(R, L, (k0 + k)) * (S.h * S.w);
   if (w_in_smem)
     for (int i = threadIdx.x; i < n_w; i += blockDim.x) cp_async4(ws + i, arena + w0 + i);
   if (s_in_smem)
@@ -486,15 +521,15 @@ __device__ __forceinline__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R,
   for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const int d = q / hw, pix = q % hw;
     const int r = pix / L.w, c = pix % L.w;
-    const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
-    const float* w = wbase + (__ldg(TB(L, fwd_widx) + (kb)) - w0);
+    const int kb = t_fwd_off(R, L, (d)), ke = t_fwd_off(R, L, (d + 1));
+    const float* w = wbase + (t_fwd_widx(R, L, (kb)) - w0);
     float acc = w[(ke - kb) * kk];                    // bias slot follows the blocks
     const int rc = (r * L.ty) * S.w + c * L.tx;
     if (offs) {
       acc = conv_cell<KX, KY>(acc, sbase + rc, offs + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
     } else {
       for (int k = kb; k < ke; ++k) {
-        const int so = __ldg(TB(L, fwd_src) + (k)) * (S.h * S.w);
+        const int so = t_fwd_src(R, L, (k)) * (S.h * S.w);
         acc = conv_cell<KX, KY>(acc, sbase + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
       }
     }
@@ -561,12 +596,12 @@ __device__ __forceinline__ float conv_value_global(const NetPtr& R, const LayerD
                                                    const float* arena, const float* src,
                                                    int d, int r, int c) {
   const int kk = L.kx * L.ky;
-  const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
-  const float* w = arena + __ldg(TB(L, fwd_widx) + (kb));
-  float acc = arena[__ldg(TB(L, bias_off) + (d))];
+  const int kb = t_fwd_off(R, L, (d)), ke = t_fwd_off(R, L, (d + 1));
+  const float* w = arena + t_fwd_widx(R, L, (kb));
+  float acc = arena[t_bias_off(R, L, (d))];
   const int rc = (r * L.ty) * S.w + c * L.tx;
   for (int k = kb; k < ke; ++k) {
-    const int so = __ldg(TB(L, fwd_src) + (k)) * (S.h * S.w);
+    const int so = t_fwd_src(R, L, (k)) * (S.h * S.w);
     acc = conv_cell<KX, KY>(acc, src + rc, &so, w + (k - kb) * kk, 1, S.w, L.kx, L.ky);
   }
   return acc;
@@ -599,7 +634,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     }
   } else if (sp.b < sp.e && S.cells <= tm.smem_floats / 2) {
     // the whole source layer, unless this CTA's maps connect to fewer cells
-    const int nk_all = __ldg(TB(L, fwd_off) + ((sp.e - 1) / phw + 1)) - __ldg(TB(L, fwd_off) + (sp.b / phw));
+    const int nk_all = t_fwd_off(R, L, ((sp.e - 1) / phw + 1)) - t_fwd_off(R, L, (sp.b / phw));
     CK_SUBT(tm, 20);
     if (S.cells <= nk_all * shw) src = stage(src, S.cells, tm, used);
     CK_SUBT(tm, 21);
@@ -619,7 +654,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     bool wst = false, slots = false;
     for (int tries = 0; tries < 24; ++tries) {
       const int d0 = q / phw, d1 = (qe - 1) / phw;
-      const int nk = __ldg(TB(L, fwd_off) + (d1 + 1)) - __ldg(TB(L, fwd_off) + (d0));
+      const int nk = t_fwd_off(R, L, (d1 + 1)) - t_fwd_off(R, L, (d0));
       const int nw = nk * kk + d1 + 1 - d0;
       const int base = ((nk + 3) & ~3) + ((nw + 3) & ~3) + (qe - q) * blk;
       if (!whole && base + nk * shw <= avail) { wst = slots = true; break; }
@@ -632,7 +667,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     }
     CK_SUBT(tm, 2);
     const int d0 = q / phw, d1 = (qe - 1) / phw;
-    const int k0 = __ldg(TB(L, fwd_off) + (d0)), k1 = __ldg(TB(L, fwd_off) + (d1 + 1));
+    const int k0 = t_fwd_off(R, L, (d0)), k1 = t_fwd_off(R, L, (d1 + 1));
     const int w0 = k0 * kk + d0;
     const int nw = (k1 - k0) * kk + d1 + 1 - d0;
     int* soff = reinterpret_cast<int*>(tm.smem + used);
@@ -644,10 +679,10 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
       int u2 = used + ((k1 - k0 + 3) & ~3);
       stage(arena + w0, nw, tm, u2);
       for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x)
-        soff[k] = slots ? k * shw : __ldg(TB(L, fwd_src) + (k0 + k)) * shw;
+        soff[k] = slots ? k * shw : t_fwd_src(R, L, (k0 + k)) * shw;
       if (slots)
         for (int k = (threadIdx.x >> 5); k < k1 - k0; k += (blockDim.x >> 5)) {
-          const float* from = src_g + __ldg(TB(L, fwd_src) + (k0 + k)) * shw;
+          const float* from = src_g + t_fwd_src(R, L, (k0 + k)) * shw;
           for (int i = lane_id(); i < shw; i += 32) cp_async4(sslot + k * shw + i, from + i);
         }
     }
@@ -662,7 +697,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
       const int c = (pp % P.w) * P.px + t % P.px;
       float acc;
       if (wst) {
-        const int kb = __ldg(TB(L, fwd_off) + (d)), ke = __ldg(TB(L, fwd_off) + (d + 1));
+        const int kb = t_fwd_off(R, L, (d)), ke = t_fwd_off(R, L, (d + 1));
         const float* w = ws + (kb * kk + d - w0);
         if constexpr (KX > 0) {
           if (whole || slots)   // weights, offsets and sources all in shared memory
@@ -968,9 +1003,9 @@ __device__ __forceinline__ void wgrad_pair(const NetPtr& R, const LayerDev& L, c
                                            float* g, bool upd, float eta_f) {
   const int lane = lane_id();
   const int hw = L.h * L.w;
-  const float* d = dl + __ldg(TB(L, pair_dst) + (p)) * hw;
-  const float* s = ys + __ldg(TB(L, fwd_src) + (p)) * (S.h * S.w);
-  const int o = __ldg(TB(L, fwd_widx) + (p));
+  const float* d = dl + t_pair_dst(R, L, (p)) * hw;
+  const float* s = ys + t_fwd_src(R, L, (p)) * (S.h * S.w);
+  const int o = t_fwd_widx(R, L, (p));
   if constexpr (KX > 0) {
     constexpr int KK = KX * KY;
     double part[KK];
@@ -1142,8 +1177,8 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   for (int c0 = ts.b; c0 < p1;) {
     int c1 = p1, da, db, need;
     for (;;) {
-      da = __ldg(TB(L, pair_dst) + (c0));
-      db = __ldg(TB(L, pair_dst) + (c1 - 1));
+      da = t_pair_dst(R, L, (c0));
+      db = t_pair_dst(R, L, (c1 - 1));
       need = 2 * (db - da + 1) * phw + (c1 - c0) * shw + 8 +
              (split > 1 ? 2 * (c1 - c0) * split * kk + 4 : 0);
       if (need <= cap || c1 - c0 == 1) break;
@@ -1160,7 +1195,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
       wdd = stage(wdd, (db - da + 1) * phw, tm, used);
       slots = tm.smem + used;
       for (int p = c0 + warp; p < c1; p += nwarps) {   // one warp per pair's source map
-        const float* from = ys_g + __ldg(TB(L, fwd_src) + (p)) * shw;
+        const float* from = ys_g + t_fwd_src(R, L, (p)) * shw;
         float* to = slots + (p - c0) * shw;
         for (int i = lane; i < shw; i += 32) cp_async4(to + i, from + i);
       }
@@ -1176,9 +1211,9 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
     }
     for (int task = warp; task < (c1 - c0) * split; task += nwarps) {
       const int p = c0 + task / split, ch = task % split;
-      const int off = (__ldg(TB(L, pair_dst) + (p)) - da) * phw;
-      const float* sp = fits ? slots + (p - c0) * shw : ys_g + __ldg(TB(L, fwd_src) + (p)) * shw;
-      wgrad_sparse(L, S, __ldg(TB(L, fwd_widx) + (p)), wr + off, wdd + off, sp, ch * phw / split,
+      const int off = (t_pair_dst(R, L, (p)) - da) * phw;
+      const float* sp = fits ? slots + (p - c0) * shw : ys_g + t_fwd_src(R, L, (p)) * shw;
+      wgrad_sparse(L, S, t_fwd_widx(R, L, (p)), wr + off, wdd + off, sp, ch * phw / split,
                    (ch + 1) * phw / split, parts ? parts + task * kk : nullptr, arena, g,
                    upd, eta_f);
     }
@@ -1189,7 +1224,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
         const int pi = e / kk, t = e % kk;
         double sum = 0.0;
         for (int ch = 0; ch < split; ++ch) sum += parts[(pi * split + ch) * kk + t];
-        emit_wg(__ldg(TB(L, fwd_widx) + (c0 + pi)), t, sum, nullptr, arena, g, upd, eta_f);
+        emit_wg(t_fwd_widx(R, L, (c0 + pi)), t, sum, nullptr, arena, g, upd, eta_f);
       }
       __syncthreads();
     }
@@ -1203,7 +1238,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
     for (int wq = lane; wq < phw; wq += 32) acc += (double)wd_g[d * phw + wq];
     acc = warp_sum(acc);
     if (lane == 0) {
-      const int o = __ldg(TB(L, bias_off) + (d));
+      const int o = t_bias_off(R, L, (d));
       if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
       else g[o] = (float)acc;
     }
@@ -1225,10 +1260,10 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   const int per_map = NS * shw * 2;                 // stream buffers (floats)
   for (int m0 = ms.b; m0 < ms.e;) {
     int m1 = min(ms.e, m0 + max(1, nwarps / NCH));
-    int ka = __ldg(TB(L, bwd_off) + (m0)), kb = __ldg(TB(L, bwd_off) + (m1));
+    int ka = t_bwd_off(R, L, (m0)), kb = t_bwd_off(R, L, (m1));
     while (m1 - m0 > 1 && (m1 - m0) * per_map + (kb - ka) * (kk + 2 * phw) > cap) {
       --m1;
-      kb = __ldg(TB(L, bwd_off) + (m1));
+      kb = t_bwd_off(R, L, (m1));
     }
     const int bufs = (m1 - m0) * per_map;
     const bool fits = bufs + (kb - ka) * (kk + 2 * phw) <= cap;
@@ -1239,9 +1274,9 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
     for (int i = threadIdx.x; i < bufs / 2; i += blockDim.x) buf[i] = 0.0;
     if (fits) {
       for (int k = ka + warp; k < kb; k += nwarps) {   // one warp per backward entry
-        const float* wfrom = arena + __ldg(TB(L, bwd_widx) + (k));
+        const float* wfrom = arena + t_bwd_widx(R, L, (k));
         for (int i = lane; i < kk; i += 32) cp_async4(wst + (k - ka) * kk + i, wfrom + i);
-        const int d = __ldg(TB(L, bwd_dst) + (k));
+        const int d = t_bwd_dst(R, L, (k));
         for (int i = lane; i < phw; i += 32) {
           cp_async4(wrs + (k - ka) * phw + i, wrc_g + d * phw + i);
           cp_async4(wds + (k - ka) * phw + i, wd_g + d * phw + i);
@@ -1254,7 +1289,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
     const int grp = kk >= 32 ? 0 : lane / kk;
     for (int task = warp; task < (m1 - m0) * NCH; task += nwarps) {
       const int mi = task / NCH, ch = task % NCH;
-      const int k0m = __ldg(TB(L, bwd_off) + (m0 + mi)), nkm = __ldg(TB(L, bwd_off) + (m0 + mi + 1)) - k0m;
+      const int k0m = t_bwd_off(R, L, (m0 + mi)), nkm = t_bwd_off(R, L, (m0 + mi + 1)) - k0m;
       const int kc0 = k0m + ch * nkm / NCH, kc1 = k0m + (ch + 1) * nkm / NCH;
       for (int t0 = 0; t0 < kk; t0 += 32) {
         const int t = kk >= 32 ? t0 + lane : lane % kk;
@@ -1270,8 +1305,8 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
             wr = wrs + (k - ka) * phw;
             wdd = wds + (k - ka) * phw;
           } else {
-            const int d = __ldg(TB(L, bwd_dst) + (k));
-            wk = arena + __ldg(TB(L, bwd_widx) + (k));
+            const int d = t_bwd_dst(R, L, (k));
+            wk = arena + t_bwd_widx(R, L, (k));
             wr = wrc_g + d * phw;
             wdd = wd_g + d * phw;
           }
@@ -1337,7 +1372,7 @@ __device__ __forceinline__ void op_conv_bwd(const NetGeo& N, const NetPtr& R, co
       for (int i = lane; i < hw; i += 32) acc += (double)dd[i];
       acc = warp_sum(acc);
       if (lane == 0) {
-        const int o = __ldg(TB(L, bias_off) + (d));
+        const int o = t_bias_off(R, L, (d));
         if (upd) arena[o] = sgd(arena[o], eta_f, (float)acc);
         else g[o] = (float)acc;
       }
@@ -1358,18 +1393,18 @@ __device__ __forceinline__ void op_conv_bwd(const NetGeo& N, const NetPtr& R, co
       // cell, so four destinations share one loop nest: accumulator q takes
       // the destinations k = kb + q (mod 4), combined in fixed order.
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      const int kb = __ldg(TB(L, bwd_off) + (s)), k1 = __ldg(TB(L, bwd_off) + (s + 1));
+      const int kb = t_bwd_off(R, L, (s)), k1 = t_bwd_off(R, L, (s + 1));
       const int dw0 = (j - ylo * L.ty) * L.kx + i - xlo * L.tx;   // weight index at (ylo, xlo)
       int k = kb;
       for (; k + 4 <= k1; k += 4) {
-        const float* d0 = dl + __ldg(TB(L, bwd_dst) + (k)) * hw + ylo * L.w;
-        const float* d1 = dl + __ldg(TB(L, bwd_dst) + (k + 1)) * hw + ylo * L.w;
-        const float* d2 = dl + __ldg(TB(L, bwd_dst) + (k + 2)) * hw + ylo * L.w;
-        const float* d3 = dl + __ldg(TB(L, bwd_dst) + (k + 3)) * hw + ylo * L.w;
-        const float* w0 = arena + __ldg(TB(L, bwd_widx) + (k)) + dw0;
-        const float* w1 = arena + __ldg(TB(L, bwd_widx) + (k + 1)) + dw0;
-        const float* w2 = arena + __ldg(TB(L, bwd_widx) + (k + 2)) + dw0;
-        const float* w3 = arena + __ldg(TB(L, bwd_widx) + (k + 3)) + dw0;
+        const float* d0 = dl + t_bwd_dst(R, L, (k)) * hw + ylo * L.w;
+        const float* d1 = dl + t_bwd_dst(R, L, (k + 1)) * hw + ylo * L.w;
+        const float* d2 = dl + t_bwd_dst(R, L, (k + 2)) * hw + ylo * L.w;
+        const float* d3 = dl + t_bwd_dst(R, L, (k + 3)) * hw + ylo * L.w;
+        const float* w0 = arena + t_bwd_widx(R, L, (k)) + dw0;
+        const float* w1 = arena + t_bwd_widx(R, L, (k + 1)) + dw0;
+        const float* w2 = arena + t_bwd_widx(R, L, (k + 2)) + dw0;
+        const float* w3 = arena + t_bwd_widx(R, L, (k + 3)) + dw0;
         for (int y = ylo; y <= yhi; ++y) {
           for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx) {
             acc[0] += (double)__fmul_rn(d0[x], w0[wi]);
@@ -1382,8 +1417,8 @@ __device__ __forceinline__ void op_conv_bwd(const NetGeo& N, const NetPtr& R, co
         }
       }
       for (; k < k1; ++k) {
-        const float* d = dl + __ldg(TB(L, bwd_dst) + (k)) * hw + ylo * L.w;
-        const float* w = arena + __ldg(TB(L, bwd_widx) + (k)) + dw0;
+        const float* d = dl + t_bwd_dst(R, L, (k)) * hw + ylo * L.w;
+        const float* w = arena + t_bwd_widx(R, L, (k)) + dw0;
         double part = 0.0;
         for (int y = ylo; y <= yhi; ++y, d += L.w, w -= L.ty * L.kx)
           for (int x = xlo, wi = 0; x <= xhi; ++x, wi -= L.tx)

@@ -562,6 +562,13 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
       cursor += 1;
       N.L[k].max_fan_in = std::max(N.L[k].max_fan_in, fwd_off[d + 1] - fwd_off[d]);
     }
+    // full table in ConnectionTable order: entries become arithmetic on device
+    {
+      bool full = D.n_pairs == L.maps * n_src;
+      for (int p = 0; full && p < D.n_pairs; ++p)
+        full = fwd_src[p] == p % n_src && pair_dst[p] == p / n_src;
+      N.L[k].full = full ? 1 : 0;
+    }
     // backward CSR = exact transpose, destinations ascending (topology.invert_table)
     bwd_off[0] = 0;
     for (int s = 0; s < n_src; ++s) bwd_off[s + 1] = bwd_off[s] + count[s];
