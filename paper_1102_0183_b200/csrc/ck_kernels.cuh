@@ -270,8 +270,12 @@ struct SpecPhases {
   }
 };
 
+#ifndef CK_SPEC_THREADS
+#define CK_SPEC_THREADS 512   // threads per CTA of the specialised kernels
+#endif
+
 template <class Spec, class Team>
-__global__ void __launch_bounds__(CK_TEAM_THREADS, 1)
+__global__ void __launch_bounds__(CK_SPEC_THREADS, 1)
 net_spec_kernel(NetRefs nets, Job job, int ctas) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned rank, team, tsize;

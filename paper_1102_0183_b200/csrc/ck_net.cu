@@ -319,6 +319,8 @@ int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
     bool same = true;
     for (int i = 0; i < n_nets; ++i)
       same = same && nets[i]->spec == nets[0]->spec && nets[i]->use_spec;
+    // an explicit team must match the specialised kernel's block size
+    same = same && (nets[0]->team_kind == CK_TEAM_AUTO || t0.threads == CK_SPEC_THREADS);
     if (same) {
       int n_spec = 0;
       spec_kernel = spec_table(&n_spec)[nets[0]->spec].kernel;
@@ -326,6 +328,7 @@ int launch_teams(ck_net* const* nets, int n_nets, Job job, cudaStream_t st) {
       if (rc) return rc;
     }
   }
+  if (spec_kernel && nets[0]->team_kind == CK_TEAM_AUTO) cfg.blockDim = dim3(CK_SPEC_THREADS);
   if (t0.kind == CK_TEAM_GRID) {
     for (int i = 0; i < n_nets; ++i) {   // arrival counters start at 0 every launch
       e = cudaMemsetAsync(nets[i]->d_bar, 0, 2 * sizeof(unsigned), st);
