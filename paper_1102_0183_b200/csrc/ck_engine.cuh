@@ -178,6 +178,7 @@ struct Job {
   int32_t* pred;           // eval
   float* outputs;          // eval (nullable)
   float* eval_scratch;     // eval: per-CTA act arenas
+  int eval_floats;         // eval: shared-memory staging per CTA (floats)
   long long* prof;         // phase end times (globaltimer ns), nullable
   int64_t prof_images;     // images profiled
   long long* sub;          // sub-phase timers (ck_debug_subprof), nullable
@@ -478,6 +479,37 @@ __device__ __forceinline__ float conv_cell_smem(float acc, const float* src, con
   return acc;
 }
 
+// All PB x PB conv cells of one pool block, one thread: the block shares its
+// dest map's weights (one load per tap for PB*PB chains) and its source
+// window (loads shared between neighbouring cells).  Each cell's own chain
+// keeps the reference order (bias, k, v, u) -- bit-identical to conv_cell.
+// For throughput (many cells per CTA: evaluation, wide first layers).
+template <int KX, int KY, int PB>
+__device__ __forceinline__ void conv_block_smem(float* acc, const float* src, const int* soff,
+                                                const float* w, int nk, int sw, int ty,
+                                                int tx) {
+  constexpr int KK = KX * KY;
+  const unsigned s0 = (unsigned)__cvta_generic_to_shared(src);
+  const unsigned o0 = (unsigned)__cvta_generic_to_shared(soff);
+  const unsigned w0 = (unsigned)__cvta_generic_to_shared(w);
+  for (int k = 0; k < nk; ++k) {
+    const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0 + 4u * k);
+#pragma unroll
+    for (int v = 0; v < KY; ++v)
+#pragma unroll
+      for (int u = 0; u < KX; ++u) {
+        const float wv = lds_f32(w0 + 4u * (k * KK + v * KX + u));
+#pragma unroll
+        for (int cy = 0; cy < PB; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < PB; ++cx) {
+            const float x = lds_f32(sb + 4u * ((cy * ty + v) * sw + cx * tx + u));
+            acc[cy * PB + cx] = __fadd_rn(acc[cy * PB + cx], __fmul_rn(wv, x));
+          }
+      }
+  }
+}
+
 // The team's cells are split into one contiguous chunk per CTA.  The chunk's
 // weights (contiguous in the arena: per dest [blocks..., bias]) and source
 // map offsets are staged in shared memory; the source layer too when it fits.
@@ -690,6 +722,47 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     stage_sync();
     CK_SUBT(tm, 4);
     const int n_items = (qe - q) * blk;
+    if constexpr (KX > 0) {
+      // many cells per thread: one pool block per thread (conv_block_smem)
+      if (wst && (whole || slots) && P.px == P.py && P.px >= 2 && P.px <= 4 &&
+          n_items > 2 * (int)blockDim.x) {
+        for (int qi = threadIdx.x; qi < qe - q; qi += blockDim.x) {
+          const int qq = q + qi;
+          const int d = qq / phw, pp = qq % phw;
+          const int r0 = (pp / P.w) * P.py, c0 = (pp % P.w) * P.px;
+          const int kb = t_fwd_off(R, L, d), ke = t_fwd_off(R, L, d + 1);
+          const float* w = ws + (kb * kk + d - w0);
+          const float* sp = sbase + (r0 * L.ty) * S.w + c0 * L.tx;
+          float acc[16];
+          const float bias = w[(ke - kb) * kk];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) acc[t] = bias;
+          if (P.px == 2)
+            conv_block_smem<KX, KY, 2>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
+          else if (P.px == 3)
+            conv_block_smem<KX, KY, 3>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
+          else
+            conv_block_smem<KX, KY, 4>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
+          int bt = 0;
+          float best = 0.0f;
+          for (int t = 0; t < blk; ++t) {   // scan order: rows, then columns
+            const int cell = d * hw + (r0 + t / P.px) * L.w + c0 + t % P.px;
+            const float yv = conv_act(acc[t]);
+            a[cell] = acc[t];
+            y[cell] = yv;
+            if (zero) dl[cell] = 0.0f;
+            if (t == 0 || yv > best) { best = yv; bt = t; }
+          }
+          const int r = r0 + bt / P.px, c = c0 + bt % P.px;
+          pyv[qq] = best;
+          parg[qq] = d * hw + r * L.w + c;
+          pwrc[qq] = (r << 16) | c;
+        }
+        __syncthreads();
+        q = qe;
+        continue;
+      }
+    }
     for (int it = threadIdx.x; it < n_items; it += blockDim.x) {
       const int qq = q + it / blk, t = it % blk;
       const int d = qq / phw, pp = qq % phw;

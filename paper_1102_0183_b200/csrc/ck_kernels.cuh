@@ -119,7 +119,8 @@ __device__ __forceinline__ long long globaltimer() {
 constexpr size_t kDescBytes = (sizeof(NetGeo) + 15) & ~size_t(15);
 constexpr size_t kScratchBytes = kScratchDoubles * sizeof(double);
 constexpr int kTeamStageFloats = 48 * 1024;   // 192 KB staging per CTA
-constexpr int kEvalStageFloats = 12 * 1024;   // 48 KB staging per CTA
+constexpr int kEvalStageFloats = 24 * 1024;   // 96 KB staging: 2 eval CTAs per SM
+constexpr int kEvalBigFloats = 48 * 1024;     // 192 KB: 1 eval CTA per SM (wide nets)
 
 // Where this CTA sits: its team (net) and rank.
 template <class Team>
@@ -233,29 +234,29 @@ net_team_kernel(NetRefs nets, Job job, int ctas) {
 // only the code the net needs.  Same ops, same arithmetic as the generic
 // kernel -- results are bit-identical (tests/test_gpu_parity.py).
 
-template <class Spec, int PH, int O>
+template <class Spec, int PROG, int PH, int O>
 struct SpecOps {
   __device__ static __forceinline__ void run(const NetPtr& R, const Job& job, Ctx& ctx,
                                              const TeamCtx& tm, double* scratch) {
-    if constexpr (O < Spec::geo().prog[PROG_TRAIN].begin[PH + 1]) {
-      constexpr Op op = Spec::geo().prog[PROG_TRAIN].ops[O];
+    if constexpr (O < Spec::geo().prog[PROG].begin[PH + 1]) {
+      constexpr Op op = Spec::geo().prog[PROG].ops[O];
       run_op(Spec::dev(), R, op, job, ctx, tm, scratch);
-      SpecOps<Spec, PH, O + 1>::run(R, job, ctx, tm, scratch);
+      SpecOps<Spec, PROG, PH, O + 1>::run(R, job, ctx, tm, scratch);
     }
   }
 };
 
-template <class Spec, int PH>
+template <class Spec, int PROG, int PH>
 struct SpecPhase {
   template <class After>
   __device__ static __forceinline__ void run(const NetPtr& R, const Job& job, Ctx& ctx,
                                              TeamCtx& tm, double* scratch, After& after) {
-    if constexpr (PH < Spec::geo().prog[PROG_TRAIN].n_phases) {
+    if constexpr (PH < Spec::geo().prog[PROG].n_phases) {
       tm.ph = PH;
       CK_SUBT(tm, 0);
-      SpecOps<Spec, PH, Spec::geo().prog[PROG_TRAIN].begin[PH]>::run(R, job, ctx, tm, scratch);
+      SpecOps<Spec, PROG, PH, Spec::geo().prog[PROG].begin[PH]>::run(R, job, ctx, tm, scratch);
       after(PH);
-      SpecPhase<Spec, PH + 1>::run(R, job, ctx, tm, scratch, after);
+      SpecPhase<Spec, PROG, PH + 1>::run(R, job, ctx, tm, scratch, after);
     }
   }
 };
@@ -266,9 +267,26 @@ struct SpecPhases {
   template <class After>
   __device__ __forceinline__ void operator()(const Job& job, Ctx& ctx, TeamCtx& tm,
                                              double* scratch, After& after) const {
-    SpecPhase<Spec, 0>::run(R, job, ctx, tm, scratch, after);
+    SpecPhase<Spec, PROG_TRAIN, 0>::run(R, job, ctx, tm, scratch, after);
   }
 };
+
+template <class Spec>
+struct SpecEval {
+  const NetPtr& R;
+  __device__ __forceinline__ void operator()(const Job& job, Ctx& ctx, TeamCtx& tm) const {
+    auto sync = [](int) { __syncthreads(); };
+    SpecPhase<Spec, PROG_EVAL, 0>::run(R, job, ctx, tm, nullptr, sync);
+  }
+};
+
+// The specialised evaluation kernel (same eval_loop as net_eval_kernel).
+template <class Spec>
+__global__ void __launch_bounds__(256)
+net_eval_spec_kernel(const NetGeo* net, NetPtr R, Job job) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  eval_loop(Spec::dev(), job, smem + kDescBytes, SpecEval<Spec>{R});
+}
 
 #ifndef CK_SPEC_THREADS
 #define CK_SPEC_THREADS 512   // threads per CTA of the specialised kernels
@@ -286,18 +304,15 @@ net_spec_kernel(NetRefs nets, Job job, int ctas) {
                   Spec::geo().prog[PROG_TRAIN].n_phases, SpecPhases<Spec>{R});
 }
 
-#ifndef CK_SPEC_UNIT   // generic-only kernels live in ck_net.cu
 // ---------------------------------------------------------------------------
 // batched evaluation: every CTA is its own team with a private act arena and
 // runs PROG_EVAL on images first+blockIdx.x, first+blockIdx.x+gridDim.x, ...
 // Same per-neuron arithmetic as training's forward, so labels are identical.
-
-__global__ void __launch_bounds__(256)
-net_eval_kernel(const NetGeo* net, NetPtr R, Job job) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  NetGeo& N = *reinterpret_cast<NetGeo*>(smem);
-  load_desc(&N, net);
-  const Program& P = N.prog[PROG_EVAL];
+// RunEval(job, ctx, tm) runs the program's phases for one image (interpreted
+// or, in the specialised kernels, unrolled at compile time).
+template <class RunEval>
+__device__ __forceinline__ void eval_loop(const NetGeo& N, const Job& job, unsigned char* work,
+                                          const RunEval& run) {
   TeamCtx tm;
   tm.ph = 0;
   tm.sub = nullptr;
@@ -308,8 +323,8 @@ net_eval_kernel(const NetGeo* net, NetPtr R, Job job) {
   tm.gsize = blockDim.x;
   tm.gwarp = threadIdx.x >> 5;
   tm.gwarps = blockDim.x >> 5;
-  tm.smem = reinterpret_cast<float*>(smem + kDescBytes);
-  tm.smem_floats = kEvalStageFloats;
+  tm.smem = reinterpret_cast<float*>(work);
+  tm.smem_floats = job.eval_floats;
   Ctx ctx;
   ctx.act = job.eval_scratch + (int64_t)blockIdx.x * N.act_size;
   const LayerDev& O = N.L[N.n_layers - 1];
@@ -317,10 +332,7 @@ net_eval_kernel(const NetGeo* net, NetPtr R, Job job) {
     ctx.t = t;
     ctx.img = job.first + t;
     set_input(N, job, ctx, tm);
-    for (int ph = 0; ph < P.n_phases; ++ph) {
-      run_phase(N, R, P, ph, job, ctx, tm, nullptr);
-      __syncthreads();
-    }
+    run(job, ctx, tm);
     const float* y = ctx.act + O.y_off;
     if (threadIdx.x == 0) {
       // numpy argmax: first maximum; a NaN wins at its first occurrence
@@ -338,6 +350,26 @@ net_eval_kernel(const NetGeo* net, NetPtr R, Job job) {
   }
 }
 
+#ifndef CK_SPEC_UNIT   // generic-only kernels live in ck_net.cu
+struct InterpEval {
+  const NetGeo& N;
+  const NetPtr& R;
+  __device__ __forceinline__ void operator()(const Job& job, Ctx& ctx, TeamCtx& tm) const {
+    const Program& P = N.prog[PROG_EVAL];
+    for (int ph = 0; ph < P.n_phases; ++ph) {
+      run_phase(N, R, P, ph, job, ctx, tm, nullptr);
+      __syncthreads();
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256)
+net_eval_kernel(const NetGeo* net, NetPtr R, Job job) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  NetGeo& N = *reinterpret_cast<NetGeo*>(smem);
+  load_desc(&N, net);
+  eval_loop(N, job, smem + kDescBytes, InterpEval{N, R});
+}
 #endif  // CK_SPEC_UNIT
 
 }  // namespace ck

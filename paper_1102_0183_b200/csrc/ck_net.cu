@@ -26,7 +26,7 @@
 
 namespace ck {
 // one per spec, defined in its generated translation unit ck_spec_<name>.cu
-#define CK_SPEC_DECL(S) const void* spec_kernel_##S();
+#define CK_SPEC_DECL(S) const void* spec_kernel_##S(); const void* spec_eval_kernel_##S();
 CK_SPEC_LIST(CK_SPEC_DECL)
 #undef CK_SPEC_DECL
 }  // namespace ck
@@ -224,7 +224,15 @@ void build_programs(NetGeo& N, bool* ok) {
 }
 
 size_t team_smem_bytes() { return kDescBytes + kScratchBytes + kTeamStageFloats * sizeof(float); }
-size_t eval_smem_bytes() { return kDescBytes + kEvalStageFloats * sizeof(float); }
+size_t eval_smem_bytes(int floats = kEvalBigFloats) { return kDescBytes + floats * sizeof(float); }
+
+// Wide nets (a source layer beyond half the 2-CTA budget) evaluate with one
+// CTA per SM and the whole shared memory; the rest with two.
+int eval_floats_for(const NetGeo& N) {
+  int widest = 0;
+  for (int k = 1; k < N.n_layers; ++k) widest = std::max(widest, N.L[k].src_cells);
+  return widest > kEvalStageFloats / 2 ? kEvalBigFloats : kEvalStageFloats;
+}
 
 int configure_kernels() {
   static bool done = false;
@@ -246,12 +254,14 @@ int configure_kernels() {
 struct SpecEntry {
   const char* name;
   NetGeo geo;
-  const void* kernel;   // net_spec_kernel<Spec, GridTeam>
+  const void* kernel;        // net_spec_kernel<Spec, GridTeam>
+  const void* eval_kernel;   // net_eval_spec_kernel<Spec>
 };
 
-#define CK_SPEC_ENTRY(S) {#S, S::geo(), spec_kernel_##S()},
+#define CK_SPEC_ENTRY(S) {#S, S::geo(), spec_kernel_##S(), spec_eval_kernel_##S()},
 const SpecEntry* spec_table(int* n) {
-  static const SpecEntry table[] = {CK_SPEC_LIST(CK_SPEC_ENTRY){nullptr, NetGeo{}, nullptr}};
+  static const SpecEntry table[] = {
+      CK_SPEC_LIST(CK_SPEC_ENTRY){nullptr, NetGeo{}, nullptr, nullptr}};
   *n = (int)(sizeof(table) / sizeof(table[0])) - 1;
   return table;
 }
@@ -1136,7 +1146,9 @@ int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut, int64_t fi
   if (rc) return rc;
   int sms = 148;
   CK_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, net->device));
-  const int ctas = (int)std::min<int64_t>(n, (int64_t)sms * 2);
+  const int floats = eval_floats_for(net->h);
+  const int per_sm = floats == kEvalBigFloats ? 1 : 2;
+  const int ctas = (int)std::min<int64_t>(n, (int64_t)sms * per_sm);
   if (ctas > net->eval_ctas) {
     CK_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     cudaFree(net->d_eval);
@@ -1153,8 +1165,25 @@ int ck_net_eval(ck_net* net, const uint8_t* images, const float* lut, int64_t fi
   job.pred = pred;
   job.outputs = outputs;
   job.eval_scratch = net->d_eval;
-  net_eval_kernel<<<ctas, 256, eval_smem_bytes(), (cudaStream_t)stream>>>(net->d_desc, net->ptr,
-                                                                          job);
+  job.eval_floats = floats;
+  if (net->spec >= 0 && net->use_spec) {
+    int n_spec = 0;
+    const void* k = spec_table(&n_spec)[net->spec].eval_kernel;
+    static std::vector<const void*> configured;
+    if (std::find(configured.begin(), configured.end(), k) == configured.end()) {
+      CK_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)eval_smem_bytes()));
+      configured.push_back(k);
+    }
+    const NetGeo* geo = net->d_desc;
+    NetPtr R = net->ptr;
+    void* args[] = {(void*)&geo, (void*)&R, (void*)&job};
+    CK_CUDA_TRY(cudaLaunchKernel(k, dim3(ctas), dim3(256), args, eval_smem_bytes(floats),
+                                 (cudaStream_t)stream));
+  } else {
+    net_eval_kernel<<<ctas, 256, eval_smem_bytes(floats), (cudaStream_t)stream>>>(
+        net->d_desc, net->ptr, job);
+  }
   count_launch();
   CK_CUDA_TRY(cudaGetLastError());
   return CK_OK;

@@ -350,3 +350,33 @@ def test_c2_trajectory_1000_steps_vs_reference(golden):
     pred = ck.predict_batch(net, test)
     np.testing.assert_array_equal(pred, g["test_pred"])
     net.close()
+
+
+# -- specialised kernels ------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_specialised_kernels_bit_identical_to_generic(name):
+    """The BASELINE nets train and evaluate with compile-time specialised
+    kernels; the generic interpreter must give the same bits."""
+    from paper_1102_0183_b200.configs import spec_for
+    spec = spec_for(name)
+    first = spec.layers[0]
+    n = 24 if name in ("C1", "C2") else 6
+    data = ck.make_glyph_dataset(n, spec.n_classes, first.out_width, seed=4,
+                                 channels=first.out_maps)
+    cfg = ck.TrainConfig(epochs=1, eta0=1e-3, seed=1)
+    fast = ck.NetworkState(spec, 3)
+    slow = ck.NetworkState(spec, 3)
+    slow.set_specialized(False)
+    assert fast.kernel_info() == f"specialised:Spec_{name}"
+    assert slow.kernel_info() == "generic"
+    m_fast = ck.train_epoch(fast, data, cfg, 0)
+    m_slow = ck.train_epoch(slow, data, cfg, 0)
+    assert m_fast == m_slow
+    np.testing.assert_array_equal(fast.flat_parameters(), slow.flat_parameters())
+    p_fast, o_fast = ck.predict_batch(fast, data, outputs=True)
+    p_slow, o_slow = ck.predict_batch(slow, data, outputs=True)
+    np.testing.assert_array_equal(p_fast, p_slow)
+    np.testing.assert_array_equal(o_fast, o_slow)
+    fast.close()
+    slow.close()
