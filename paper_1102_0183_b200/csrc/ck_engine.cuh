@@ -222,6 +222,7 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
       long long _t;                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                  \
       (tm).sub[(tm).ph * 32 + (i)] = _t;                                      \
+      if ((i) == 0) (tm).sub[(tm).ph * 32 + 28] = clock64();                  \
     }                                                                         \
   } while (0)
 

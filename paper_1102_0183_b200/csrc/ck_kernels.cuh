@@ -176,6 +176,8 @@ __device__ __forceinline__ void team_loop(const NetGeo& N, const NetPtr& R, cons
     if (prof && rank == 0 && threadIdx.x == 0) prof[0] = globaltimer();
     auto after_phase = [&](int ph) {
       CK_SUBT(tm, 30);
+      if (tm.sub && threadIdx.x == 0 && tm.rank == tm.sub_rank)
+        tm.sub[ph * 32 + 29] = clock64();   // SM cycles at the same point (clock check)
       if (prof) {
         __syncthreads();
         if (threadIdx.x == 0) prof[1 + ph * (1 + tsize) + 1 + rank] = globaltimer();

@@ -33,9 +33,13 @@ for rank in ranks:
     print(f"== {name} rank {rank}")
     for ph, line in enumerate(prog):
         row = b[ph]
-        pts = [(i, int(row[i])) for i in range(32) if row[i]]
+        pts = [(i, int(row[i])) for i in range(28) if row[i]] + \
+              [(i, int(row[i])) for i in (30, 31) if row[i]]
         if not pts:
             continue
         t0 = pts[0][1]
         segs = " ".join(f"{i}:{(t - t0) / 1e3:.2f}" for i, t in pts[1:])
-        print(f"  {line[:60]:60s} | {segs}")
+        clk = ""
+        if row[28] and row[29] and row[30] and row[0]:
+            clk = f" | SM clock {(row[29] - row[28]) / max(1, row[30] - row[0]):.2f} GHz"
+        print(f"  {line[:60]:60s} | {segs}{clk}")
