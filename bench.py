@@ -64,6 +64,7 @@ def parse_args(argv=None):
                     help="bounded CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-committee", action="store_true")
     return ap.parse_args(argv)
 
 
@@ -231,8 +232,10 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
+    import ctypes as C
+
     import paper_1102_0183_b200 as ck
-    from paper_1102_0183_b200 import _lib, training
+    from paper_1102_0183_b200 import _lib, multigpu, training
     from paper_1102_0183_b200.configs import DESCRIPTION, spec_for, work_per_image
     from paper_1102_0183_b200.device import DeviceDataset, pin_dataset, upload_bytes
 
@@ -366,6 +369,46 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8,
                "api": "paper_1102_0183_b200.train_epoch(net, host Dataset, config, epoch)"}
 
+    # -- committee (BASELINE configs[4]): 8 independent C1 nets over the N
+    # ranks, each rank's members trained together in one launch per step ---
+    committee = None
+    if not args.no_committee:
+        c_spec = spec_for("C1")
+        members = multigpu.nets_for_rank(8, rank, world)
+        c_nets = [ck.NetworkState(c_spec, m, device=local) for m in members]
+        c_data = make_data(c_spec, n_img, 1, "train")
+        c_dd = DeviceDataset(c_data, local)
+        handles = (C.c_void_p * len(c_nets))(*[nt.handle.value for nt in c_nets])
+
+        def committee_step(k):
+            _lib.call("ck_committee_train_epoch", handles, len(c_nets), c_dd.images_ptr,
+                      c_dd.lut_ptr, c_dd.labels.data_ptr(), orders[k % 4].data_ptr(), n_img,
+                      float(eta), None, sh)
+
+        if c_nets:
+            for w in range(args.warmup):
+                committee_step(w)
+        barrier()
+        c_ms = []
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            if c_nets:
+                committee_step(k)
+            e.record(stream)
+            e.synchronize()
+            c_ms.append(s.elapsed_time(e))
+        barrier()
+        c_total = max_over_ranks(sum(c_ms))
+        committee = {"value": 8 * n_img * args.steps / (c_total / 1e3), "unit": UNIT,
+                     "nets": 8, "nets_per_gpu": len(members), "config": "C1",
+                     "kernel": c_nets[0].kernel_info() if c_nets else None,
+                     "note": "8 independent C1 nets (seeds 0..7), one launch per rank per "
+                             "step; total online-training images/s over all nets"}
+        for nt in c_nets:
+            nt.close()
+
     # -- roofline of the persistent training kernel ------------------------
     props = torch.cuda.get_device_properties(local)
     sm_max = clk.get("sm_max_mhz") or 1965.0
@@ -414,6 +457,7 @@ def run_ours(args):
                      if world > 1 else "none (1 GPU)",
                      "eval_mflop_per_img": work["forward"] / 1e6},
             "e2e": e2e,
+            "committee": committee,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"persistent online-training kernel ({net.kernel_info()})",

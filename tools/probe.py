@@ -80,12 +80,13 @@ def main():
         ck.predict_batch(net, data.limit(10))
         ms = timed(lambda: ck.predict_batch(net, data))
         print(f"{name} eval: {ms:.2f} ms / {n} -> {n / ms * 1e3:.0f} img/s", flush=True)
-        if name == "C1":
-            for k in (4, 8):
-                nets = [ck.NetworkState(spec, s, team=(1, 16, 512)) for s in range(k)]
+        if name in ("C1", "C2"):
+            for k in (2, 4, 8):
+                nets = [ck.NetworkState(spec, s) for s in range(k)]
                 ck.train_committee_epoch(nets, data.limit(20), cfg, 0)
                 ms = timed(lambda: ck.train_committee_epoch(nets, data, cfg, 0))
-                print(f"C1 committee x{k}: {ms:.2f} ms -> {k * n / ms * 1e3:.0f} img/s total",
+                print(f"{name} committee x{k} [{nets[0].kernel_info()}]: {ms:.2f} ms -> "
+                      f"{k * n / ms * 1e3:.0f} img/s total",
                       flush=True)
                 for nn in nets:
                     nn.close()
