@@ -46,7 +46,7 @@ enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
   X(int, src_maps) X(int, src_h) X(int, src_w) X(int, src_cells)             \
   X(int, kx) X(int, ky) X(int, tx) X(int, ty) X(int, px) X(int, py)          \
   X(int, n_pairs) X(int, has_delta) X(int, n_filt) X(int, fh) X(int, fw)     \
-  X(int, max_fan_in) X(int, pool_above) X(int, wg_winner_major)              \
+  X(int, max_fan_in) X(int, pool_above)                                      \
   X(int, wg_split) X(int, pull_g) X(int, pull_ch) X(int, full)               \
   X(int64_t, p_off) X(int64_t, b_off) X(int64_t, n_par)                      \
   X(int64_t, y_off) X(int64_t, a_off) X(int64_t, d_off) X(int64_t, arg_off)  \
@@ -56,8 +56,8 @@ enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
   X(int, o_filt)
 
 // Field notes: tx = sx + 1 (conv stride); pool_above: the next layer is a
-// max-pool (sparse backward); wg_*: weight-gradient lane layout / winner
-// chunks; pull_g / pull_ch: pull lane groups / backward-list chunks; full:
+// max-pool (sparse backward); wg_split: weight-gradient winner chunks per
+// pair; pull_g / pull_ch: pull lane groups / backward-list chunks; full:
 // the conv table is the full table in ConnectionTable's order, so every table
 // entry is arithmetic (no loads);
 // *_off: act-arena offsets (elements); wrc_off / wd_off: a pool over a conv
@@ -1129,92 +1129,19 @@ __device__ __forceinline__ void wgrad_pair(const NetPtr& R, const LayerDev& L, c
 // arrays the forward pass (winner row/col) and emit_delta (winner delta)
 // fill.  Same products, same f64 accumulation; terms that are exactly zero
 // are skipped.
-//   weight_grad  one warp per pair: lane = (tap, group); a group walks every
-//                G-th winner of the dest map; groups combined in order
+//   weight_grad  tasks = (pair, chunk of <= 32 winners); lane = (task group,
+//                tap): a lane's serial f64 sum over the chunk's winners for
+//                one tap; chunks combined in chunk order
 //   bias_grad    one warp per dest map
-//   pull_bwd     one thread per source cell: for every dest map in its
-//                backward list, the pool blocks that meet the covering window,
-//                each contributing its winner when the winner lies inside
-// Weight-gradient sums of one pair over the winners [wb, we) of its dest map.
-// Each function ends with the per-tap f64 sums; emit_wg either applies them
-// (out == nullptr: update in place or store the gradient) or parks them in
-// out[t] for a fixed-order combination with the pair's other winner chunks.
-//   wr / wdd  winner (r<<16|c) and winner delta of the pair's dest map
-//   s         the pair's source map (y of the layer below)
+//   pull_bwd     a scatter per source map into f64 stream buffers (below)
+// emit_wg applies a weight-gradient sum (out == nullptr: update in place or
+// store the gradient) or parks it in out[t] for the fixed-order combination
+// with the pair's other winner chunks.
 __device__ __forceinline__ void emit_wg(int o, int t, double sum, double* out, float* arena,
                                         float* g, bool upd, float eta_f) {
   if (out) out[t] = sum;
   else if (upd) arena[o + t] = sgd(arena[o + t], eta_f, (float)sum);
   else g[o + t] = (float)sum;
-}
-
-// Tap-major: lane = (tap, group); group gr walks winners wb+gr, wb+gr+G, ...;
-// the groups are combined in group order.
-__device__ __forceinline__ void wgrad_pair_sparse(const LayerDev& L, const LayerDev& S,
-                                                  int o, const int* wr, const float* wdd,
-                                                  const float* s, int wb, int we,
-                                                  double* out, float* arena, float* g,
-                                                  bool upd, float eta_f) {
-  const int lane = lane_id();
-  const int kk = L.kx * L.ky;
-  const int G = kk >= 32 ? 1 : 32 / kk;
-  for (int t0 = 0; t0 < kk; t0 += 32) {
-    const int t = kk >= 32 ? t0 + lane : lane % kk;
-    const int grp = kk >= 32 ? 0 : lane / kk;
-    double part = 0.0;
-    if (t < kk && grp < G) {
-      const int v = t / L.kx, u = t % L.kx;
-      const float* sv = s + v * S.w + u;
-#pragma unroll 4
-      for (int wq = wb + grp; wq < we; wq += G) {
-        const int rc = wr[wq];
-        part += (double)__fmul_rn(wdd[wq], sv[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx]);
-      }
-    }
-    double tot = part;
-    for (int gg = 1; gg < G; ++gg) tot += __shfl_sync(0xffffffffu, part, (lane + gg * kk) & 31);
-    if (grp == 0 && t < kk) emit_wg(o, t, tot, out, arena, g, upd, eta_f);
-  }
-}
-
-// Winner-major variant for maps with many winners: lanes split the winners,
-// each lane keeps kx*ky f64 partials, then one fixed xor tree per tap.
-template <int KX, int KY>
-__device__ __forceinline__ void wgrad_pair_winners(const LayerDev& L, const LayerDev& S,
-                                                   int o, const int* wr, const float* wdd,
-                                                   const float* s, int wb, int we,
-                                                   double* out, float* arena, float* g,
-                                                   bool upd, float eta_f) {
-  constexpr int KK = KX * KY;
-  const int lane = lane_id();
-  double part[KK];
-#pragma unroll
-  for (int t = 0; t < KK; ++t) part[t] = 0.0;
-  for (int wq = wb + lane; wq < we; wq += 32) {
-    const int rc = wr[wq];
-    const float dv = wdd[wq];
-    const float* base = s + (rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx;
-#pragma unroll
-    for (int t = 0; t < KK; ++t) part[t] += (double)__fmul_rn(dv, base[(t / KX) * S.w + t % KX]);
-  }
-#pragma unroll
-  for (int t = 0; t < KK; ++t) {
-    const double sum = warp_sum(part[t]);
-    if (lane == t % 32) emit_wg(o, t, sum, out, arena, g, upd, eta_f);
-  }
-}
-
-__device__ __forceinline__ void wgrad_sparse(const LayerDev& L, const LayerDev& S, int o,
-                                             const int* wr, const float* wdd, const float* s,
-                                             int wb, int we, double* out, float* arena,
-                                             float* g, bool upd, float eta_f) {
-  if (L.wg_winner_major) {
-    if (L.kx == 2 && L.ky == 2) return wgrad_pair_winners<2, 2>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
-    if (L.kx == 3 && L.ky == 3) return wgrad_pair_winners<3, 3>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
-    if (L.kx == 4 && L.ky == 4) return wgrad_pair_winners<4, 4>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
-    if (L.kx == 5 && L.ky == 5) return wgrad_pair_winners<5, 5>(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
-  }
-  wgrad_pair_sparse(L, S, o, wr, wdd, s, wb, we, out, arena, g, upd, eta_f);
 }
 
 // Each CTA stages exactly what its share needs (one cp.async round trip per
@@ -1283,13 +1210,31 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
       const int after = fits ? used + (c1 - c0) * shw : 0;
       parts = reinterpret_cast<double*>(tm.smem + ((after + 3) & ~3));
     }
-    for (int task = warp; task < (c1 - c0) * split; task += nwarps) {
+    // lane = (group, tap): a warp runs 32/kk tasks side by side, each lane a
+    // serial f64 sum over its task's winners for one tap -- no shuffles
+    const int ng = kk <= 32 ? 32 / kk : 1;
+    const int grp = kk <= 32 ? lane / kk : 0;
+    const int n_tasks = (c1 - c0) * split;
+    for (int tb = warp * ng; tb < n_tasks; tb += nwarps * ng) {
+      const int task = tb + grp;
+      if (grp >= ng || task >= n_tasks) continue;
       const int p = c0 + task / split, ch = task % split;
       const int off = (t_pair_dst(R, L, (p)) - da) * phw;
       const float* sp = fits ? slots + (p - c0) * shw : ys_g + t_fwd_src(R, L, (p)) * shw;
-      wgrad_sparse(L, S, t_fwd_widx(R, L, (p)), wr + off, wdd + off, sp, ch * phw / split,
-                   (ch + 1) * phw / split, parts ? parts + task * kk : nullptr, arena, g,
-                   upd, eta_f);
+      const int o = t_fwd_widx(R, L, (p));
+      const int wb = ch * phw / split, we = (ch + 1) * phw / split;
+      const int* wrp = wr + off;
+      const float* wdp = wdd + off;
+      for (int t = (kk <= 32 ? lane % kk : lane); t < kk; t += (kk <= 32 ? kk : 32)) {
+        const float* sv = sp + (t / L.kx) * S.w + t % L.kx;
+        double part = 0.0;
+#pragma unroll 4
+        for (int wq = wb; wq < we; ++wq) {
+          const int rc = wrp[wq];
+          part += (double)__fmul_rn(wdp[wq], sv[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx]);
+        }
+        emit_wg(o, t, part, parts ? parts + task * kk : nullptr, arena, g, upd, eta_f);
+      }
     }
     CK_SUBT(tm, 13);
     __syncthreads();

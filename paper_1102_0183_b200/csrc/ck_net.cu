@@ -432,16 +432,11 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
         // weight_grad lane layout: tap-major (lanes = taps x groups walking
         // the winners) or winner-major (lanes walk winners, per-tap partials
         // + xor trees); pick the cheaper one for this geometry
-        // maps with many winners split each pair's sum into wg_split chunks
-        // (one warp each, combined in chunk order: a geometry constant, so
-        // results never depend on the team)
+        // weight gradients: each pair's sum over its winners is cut into
+        // wg_split chunks of <= 32 winners (one lane group each, combined in
+        // chunk order: a geometry constant, so results never depend on the team)
         const int kk = C.kx * C.ky, phw = D.width * D.height;
-        C.wg_split = std::max(1, std::min(16, phw / 24));
-        const int chunk = (phw + C.wg_split - 1) / C.wg_split;
-        const int G = kk >= 32 ? 1 : std::min(32 / kk, chunk);
-        const int cost_tap = ((chunk + G - 1) / G) * 40 * ((kk + 31) / 32);
-        const int cost_win = ((chunk + 31) / 32) * kk * 3 + kk * 15;
-        C.wg_winner_major = C.kx == C.ky && C.kx >= 2 && C.kx <= 5 && cost_win < cost_tap;
+        C.wg_split = std::max(1, std::min(16, (phw + 31) / 32));
         // pull streams: lane groups (one winner each, lane = tap) x chunks of
         // the backward list, <= 16 f64 copies of a source map in shared memory
         C.pull_g = kk >= 32 ? 1 : std::min(32 / kk, phw);
