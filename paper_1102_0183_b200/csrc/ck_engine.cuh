@@ -33,6 +33,7 @@ constexpr int kMaxPhases = 56;
 constexpr int kFcSlices = 16;      // FC forward: i-slices combined in fixed order
 constexpr int kPullLanes = 8;      // pull: lanes per source cell
 constexpr int kFcTile = 8;         // FC forward: output columns per CTA tile
+constexpr int kImgLanes = 8;       // contrast layer: lanes per response cell
 constexpr int kStageMax = 4096;    // largest per-layer array every CTA copies
 
 enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
@@ -357,41 +358,67 @@ __device__ __forceinline__ void op_load_input(const NetGeo& N, const NetPtr& R, 
 }
 
 // correlate(mode="nearest") per (filter, channel): f64 sum, one rounding.
-// One warp per output cell: lanes split the taps, fixed-order xor reduction.
 __device__ __forceinline__ void op_imgproc(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                            const TeamCtx& tm) {
   __syncthreads();   // scratch reuse
+  CK_SUBT(tm, 1);
   const LayerDev& I = N.L[0];
   int used = 0;
   const float* src = stage_input(N, R, tm, used);
+  CK_SUBT(tm, 2);
   if (!src) src = act + I.y_off;   // (never: the builder folds only inputs that fit)
-  stage_sync();
   float* out = act + L.y_off;
   const int hw = L.h * L.w;
   const int C = I.maps;
-  const Span cp = cta_span(C * hw, tm);
-  for (int q = cp.b + threadIdx.x; q < cp.e; q += blockDim.x) out[q] = src[q];
   const int cy = L.fh / 2, cx = L.fw / 2;
   const int taps = L.fh * L.fw;
   const int lane = lane_id();
   const int n_resp = L.cells - C * hw;
   const Span rs = cta_span(n_resp, tm);
-  for (int r = rs.b + (threadIdx.x >> 5); r < rs.e; r += blockDim.x >> 5) {
+  // the coefficients of the filters this CTA's responses use, staged as raw
+  // 32-bit halves of the doubles (a read per tap otherwise waits on L2)
+  const double* kbase = R.filt + L.o_filt;
+  int f_lo = 0, f_hi = -1;
+  if (rs.b < rs.e) {
+    f_lo = (rs.b / hw) / C;
+    f_hi = ((rs.e - 1) / hw) / C;
+    used = (used + 1) & ~1;   // 8-byte alignment for the doubles
+    if (used + 2 * (f_hi - f_lo + 1) * taps <= tm.smem_floats) {
+      float* dst = tm.smem + used;
+      const float* from = reinterpret_cast<const float*>(kbase + (int64_t)f_lo * taps);
+      for (int i = threadIdx.x; i < 2 * (f_hi - f_lo + 1) * taps; i += blockDim.x)
+        cp_async4(dst + i, from + i);
+      kbase = reinterpret_cast<const double*>(dst) - (int64_t)f_lo * taps;
+    }
+  }
+  CK_SUBT(tm, 3);
+  stage_sync();
+  CK_SUBT(tm, 4);
+  const Span cp = cta_span(C * hw, tm);
+  for (int q = cp.b + threadIdx.x; q < cp.e; q += blockDim.x) out[q] = src[q];
+  // kImgLanes lanes per response cell: lane l takes the filter rows
+  // i = l, l + kImgLanes, ... (fma chains in f64), combined by a fixed xor
+  // tree.  The f64 result rounds to the same f32 as the reference's f64 sum
+  // (any f64 order gave 0 mismatches).
+  const int sub = threadIdx.x % kImgLanes;
+  const unsigned gmask = ((1u << kImgLanes) - 1) << (lane & ~(kImgLanes - 1));
+  for (int r = rs.b + threadIdx.x / kImgLanes; r < rs.e; r += blockDim.x / kImgLanes) {
     const int q = C * hw + r;
     const int o = q / hw, pix = q % hw;
     const int y = pix / L.w, x = pix % L.w;
     const int f = (o - C) / C, c = (o - C) % C;
     const float* s = src + c * hw;
-    const double* k = (R.filt + L.o_filt) + (int64_t)f * taps;
+    const double* k = kbase + (int64_t)f * taps;
     double acc = 0.0;
-    for (int t = lane; t < taps; t += 32) {
-      const int i = t / L.fw, j = t % L.fw;
-      const int yy = min(max(y + i - cy, 0), L.h - 1);
-      const int xx = min(max(x + j - cx, 0), L.w - 1);
-      acc = __dadd_rn(acc, __dmul_rn(__ldg(k + t), (double)s[yy * L.w + xx]));
+    for (int i = sub; i < L.fh; i += kImgLanes) {
+      const float* srow = s + min(max(y + i - cy, 0), L.h - 1) * L.w;
+      const double* krow = k + i * L.fw;
+      for (int j = 0; j < L.fw; ++j)
+        acc = fma(krow[j], (double)srow[min(max(x + j - cx, 0), L.w - 1)], acc);
     }
-    acc = warp_sum(acc);
-    if (lane == 0) out[q] = (float)acc;
+#pragma unroll
+    for (int m = kImgLanes / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(gmask, acc, m);
+    if (sub == 0) out[q] = (float)acc;
   }
 }
 
