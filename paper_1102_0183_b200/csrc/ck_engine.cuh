@@ -1024,6 +1024,8 @@ __device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, cons
   int used = 0;
   const float* x = stage(act + S.y_off, S.cells, tm, used);
   const float* W = stage(R.params + L.p_off, S.cells * L.cells, tm, used, 1 << 14);
+  // fused: H's pre-activations too (its f'(a) below), in the same round trip
+  const float* ha = (flags & F_FUSE_BELOW) ? stage(act + S.a_off, S.cells, tm, used) : nullptr;
   float* yd = tm.smem + used;                    // [a | y | delta] x n_out (+ H's deltas)
   used += (3 * L.cells + ((flags & F_FUSE_BELOW) ? S.cells : 0) + 3) & ~3;
   double* red = reinterpret_cast<double*>(tm.smem + used);
@@ -1065,23 +1067,30 @@ __device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, cons
   const LayerDev& H = S;
   float* dh = yd + 3 * L.cells;                  // H's deltas, all rows
   {
-    const int lane = lane_id(), n_out = L.cells;
+    // one thread per row of this layer's W: a serial f64 fma chain over the
+    // outputs, then f'(a) -- every CTA gets the same bits
+    const int n_out = L.cells;
     const float* dl = yd + 2 * n_out;
-    for (int i = threadIdx.x >> 5; i < H.cells; i += blockDim.x >> 5) {
+    for (int i = threadIdx.x; i < H.cells; i += blockDim.x) {
       const float* row = W + i * n_out;
       double acc = 0.0;
-      for (int j = lane; j < n_out; j += 32) acc = fma((double)row[j], (double)dl[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) dh[i] = (float)acc;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < H.cells; i += blockDim.x) {   // f'(a) in parallel
-      dh[i] = __fmul_rn(dh[i], act_deriv(act[H.a_off + i]));
+      for (int j = 0; j < n_out; ++j) acc = fma((double)row[j], (double)dl[j], acc);
+      dh[i] = __fmul_rn((float)acc, act_deriv(ha[i]));
       if (tm.rank == 0) act[H.d_off + i] = dh[i];
     }
   }
   __syncthreads();
-  fc_bwd_rows(N, R, L, li, 0, job.eta_f, act, x, yd + 2 * L.cells, tm, false);
+  {   // this layer's gradients (stored; its update is the next phase's)
+    const float* dl = yd + 2 * L.cells;
+    float* gW = R.grads + L.p_off;
+    float* gb = R.grads + L.b_off;
+    for (int j = tm.gtid; j < L.cells; j += tm.gsize) gb[j] = dl[j];
+    const Span rows = cta_span(H.cells, tm);
+    for (int e = threadIdx.x; e < (rows.e - rows.b) * L.cells; e += blockDim.x) {
+      const int i = rows.b + e / L.cells, j = e % L.cells;
+      gW[i * L.cells + j] = __fmul_rn(x[i], dl[j]);
+    }
+  }
   fc_bwd_rows(N, R, H, li - 1, flags & F_UPDATE, job.eta_f, act, act + N.L[li - 2].y_off, dh, tm);
   __syncthreads();
 }
