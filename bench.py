@@ -244,16 +244,18 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun (any world size, 1 included) the collectives run for real
+    use_dist = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ or "RANK" in os.environ
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
+        if not use_dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -307,7 +309,7 @@ def run_ours(args):
     pred = torch.zeros(per, dtype=torch.int32, device=dev)
     gathered = torch.zeros(per * world, dtype=torch.int32, device=dev)
     labels = tdd.labels
-    if world > 1:      # evaluate one committee member everywhere: rank 0's weights
+    if use_dist:       # evaluate one committee member everywhere: rank 0's weights
         flat = torch.from_numpy(net.flat_parameters()).to(dev)
         dist.broadcast(flat, 0)
         eval_net = ck.NetworkState(spec, 0, device=local)
@@ -319,7 +321,7 @@ def run_ours(args):
         if mine:
             training.eval_range_async(eval_net, tdd, first, mine, pred, stream=sh)
         wrong = (pred[:mine] != labels[first:first + mine]).sum().to(torch.int64).reshape(1)
-        if world > 1:
+        if use_dist:
             dist.all_gather_into_tensor(gathered, pred)
             dist.all_reduce(wrong)
         else:
@@ -454,7 +456,7 @@ def run_ours(args):
                      "scaling": "strong", "error_pct": err_pct,
                      "ms_per_pass": ev_total / args.steps,
                      "collectives": "nccl all_gather(labels) + all_reduce(errors)"
-                     if world > 1 else "none (1 GPU)",
+                     if use_dist else "none (single process)",
                      "eval_mflop_per_img": work["forward"] / 1e6},
             "e2e": e2e,
             "committee": committee,
@@ -468,7 +470,7 @@ def run_ours(args):
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

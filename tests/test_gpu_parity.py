@@ -7,8 +7,8 @@ Tolerance policy (stated here so the tests are the contract):
     combine partial sums in another order; the f32 result equals the
     reference's except at a rounding boundary -> rtol 2e-6.
   * FC layers: the reference uses OpenBLAS sgemv and numpy's SIMD float32
-    tanh; the device uses an f64-accumulated dot and a correctly rounded tanh
-    -> FC a / y / delta within rtol 2e-6 (a few ulp).
+    tanh; the device uses an f64-accumulated dot and CUDA's tanhf (both
+    within ~2 ulp of the true tanh) -> FC a / y / delta within rtol 2e-6.
   * weights after N online steps: max |dw| <= 1e-6 (1 step), 1e-5 (an epoch
     of small nets), 1e-4 (C2, 1000 steps; SURVEY.md §7.3 trajectory bound).
 """
