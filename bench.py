@@ -46,6 +46,7 @@ import numpy as np  # noqa: E402
 METRIC = ("online-train images/sec/GPU and eval images/sec at 1/2/4/8 B200, "
           "% roofline vs CPU")
 UNIT = "images/s"
+_OUT = sys.stdout   # the JSON line's stream (see _stdout_for_json_only)
 FP32_LANES_PER_SM = 128      # B200 SIMT FP32 lanes per SM (2 FLOP per FFMA)
 TEST_IMAGES = 10_000
 
@@ -221,7 +222,7 @@ def run_reference(args):
                                    f"threads, {cpu_model()})"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_OUT, flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -469,13 +470,25 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_OUT, flush=True)
     if use_dist:
         dist.destroy_process_group()
 
 
+def _stdout_for_json_only():
+    """Route everything native code prints (NCCL's version banner, ...) to
+    stderr; return a writer for the original stdout, which gets the JSON line
+    and nothing else."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
+
+
 def main(argv=None):
     args = parse_args(argv)
+    global _OUT
+    _OUT = _stdout_for_json_only()
     if args.impl == "reference":
         run_reference(args)
     else:
