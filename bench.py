@@ -66,6 +66,7 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-committee", action="store_true")
+    ap.add_argument("--no-deform", action="store_true")
     return ap.parse_args(argv)
 
 
@@ -412,6 +413,45 @@ def run_ours(args):
         for nt in c_nets:
             nt.close()
 
+    # -- on-line deformation (augment.py): the paper's MNIST
+    # distortions drawn and applied on the device for every image of the
+    # step, then the online pass over the deformed float32 images ----------
+    deform = None
+    if not args.no_deform:
+        from paper_1102_0183_b200 import augment
+        dcfg = augment.DeformationConfig(rotate_max=15.0, scale_max=0.15, elastic_sigma=6.0,
+                                         elastic_alpha_max=36.0 / 29.0 * 6.0)
+        dbuf = torch.empty((n_img, *dd.in_shape), dtype=torch.float32, device=dev)
+
+        def deform_step(k, train_too):
+            augment.deform_epoch(dd, dcfg, rank, k, out=dbuf, stream=sh)
+            if train_too:
+                _lib.call("ck_net_train_epoch", net.handle, dbuf.data_ptr(), None,
+                          dd.labels.data_ptr(), orders[k % 4].data_ptr(), n_img, float(eta),
+                          None, None, sh)
+
+        res = {}
+        for train_too in (False, True):
+            for w in range(args.warmup):
+                deform_step(w, train_too)
+            barrier()
+            d_ms = []
+            for k in range(args.steps):
+                flush.fill_(float(k))
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record(stream)
+                deform_step(k, train_too)
+                e.record(stream)
+                e.synchronize()
+                d_ms.append(s.elapsed_time(e))
+            barrier()
+            res[train_too] = world * n_img * args.steps / (max_over_ranks(sum(d_ms)) / 1e3)
+        deform = {"value": res[False], "unit": UNIT, "train_value": res[True],
+                  "config": "rotate 15 deg, scale 15%, elastic sigma 6 alpha 7.45 px "
+                            "(PAPER MNIST distortions), params drawn on the device",
+                  "note": "value: deformation kernel alone (images/s); train_value: "
+                          "deformation + online pass over the deformed images"}
+
     # -- roofline of the persistent training kernel ------------------------
     props = torch.cuda.get_device_properties(local)
     sm_max = clk.get("sm_max_mhz") or 1965.0
@@ -461,6 +501,7 @@ def run_ours(args):
                      "eval_mflop_per_img": work["forward"] / 1e6},
             "e2e": e2e,
             "committee": committee,
+            "deform": deform,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"persistent online-training kernel ({net.kernel_info()})",

@@ -227,6 +227,45 @@ int ck_net_kernel_info(const ck_net* net, char* buf, int cap);
  * dev_buf[phase * 32 + point] (>= 32 * n_phases int64, device); NULL disarms. */
 int ck_debug_subprof(long long* dev_buf, int rank);
 
+
+/* ------------------------------------------------------------------------
+ * 3. On-line deformation (convkit.augment, augment.py:63-170), used by
+ *    training.train_epoch when the config's deformation is enabled
+ *    (training.py:140-144).  Field meaning as augment.DeformationConfig /
+ *    DeformationParams; sigma is the config's (one per call).
+ * ---------------------------------------------------------------------- */
+typedef struct ck_deform_cfg {
+  double translate_max, rotate_max, scale_max, shear_max; /* fraction, deg, fraction, deg */
+  double elastic_sigma, elastic_alpha_max;                /* px */
+} ck_deform_cfg;
+
+typedef struct ck_deform_params {
+  double translate_x, translate_y; /* fraction of width / height */
+  double rotate;                   /* degrees, counterclockwise */
+  double scale_x, scale_y;
+  double shear_h;                  /* degrees */
+  double elastic_alpha;            /* px */
+  uint32_t seed;                   /* elastic field seed */
+  uint32_t pad;
+} ck_deform_params;
+
+/* Deform every image i < n of images (n, C, H, W) (uint8 + lut, or float32
+ * when lut is NULL) with augment.sample_params(cfg, [seed, epoch, i]) drawn on
+ * the device (numpy SeedSequence + PCG64, bit-exact) into out (n, C, H, W)
+ * float32 (device).  gauss_w: the 2*radius+1 normalised Gaussian taps of
+ * scipy's _gaussian_kernel1d(elastic_sigma, 0, int(3*sigma+0.5)) (device
+ * f64).  params_out (device, nullable) receives the drawn parameters. */
+int ck_deform_epoch(const uint8_t* images, const float* lut, int channels, int height,
+                    int width, int64_t n, const ck_deform_cfg* cfg, const double* gauss_w,
+                    int radius, uint64_t seed, uint64_t epoch, ck_deform_params* params_out,
+                    float* out, ck_stream_t stream);
+
+/* augment.deform_channels (augment.py:150-170) with explicit per-image
+ * parameters (device array of n). */
+int ck_deform_apply(const uint8_t* images, const float* lut, int channels, int height,
+                    int width, int64_t n, const ck_deform_params* params,
+                    const double* gauss_w, int radius, float* out, ck_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

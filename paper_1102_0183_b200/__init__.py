@@ -7,6 +7,8 @@ Mirrors the public API of the reference package ``convkit`` for that path
 """
 
 from .arch import parse_architecture, parse_experiment, resolve_geometry
+from .augment import (DeformationConfig, DeformationParams, deform_channels,
+                      sample_params)
 from .data import (Dataset, byte_lut, from_bytes, make_glyph_dataset,
                    make_glyph_images, normalize)
 from .errors import (ConfigError, ConvkitError, CudaError, DataFormatError,

@@ -89,6 +89,9 @@ _SIGNATURES = {
                                   C.POINTER(_i64)]),
     "ck_net_set_specialized": (_i32, [_vp, _i32]),
     "ck_net_kernel_info": (_i32, [_vp, C.c_char_p, _i32]),
+    "ck_deform_epoch": (_i32, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _i32,
+                               C.c_uint64, C.c_uint64, _vp, _vp, _vp]),
+    "ck_deform_apply": (_i32, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _i32, _vp, _vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

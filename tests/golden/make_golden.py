@@ -13,6 +13,9 @@ Writes, next to this script:
                 plus dense FC buffers
   c2_traj.npz   deep-MNIST C2: 1000 online steps, weight subsamples after
                 steps 1/10/100/1000, per-step losses (BASELINE configs[1])
+  deform.npz    augment.sample_params / deform_channels on C1/C3/C4-shaped
+                glyphs under several DeformationConfigs, and one deformed
+                online epoch of a small net (training.py:140-144)
 Large arrays are stored as sha256 digests of their float32 bytes plus
 seeded subsamples so the fixtures stay small.
 """
@@ -29,6 +32,9 @@ import numpy as np
 import convkit as ck
 from convkit import kernels
 from convkit.synth import make_glyph_images
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from cases import DEFORM_CFGS, DEFORM_SHAPES  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 F32 = np.float32
@@ -282,7 +288,41 @@ def c2_trajectory(steps=1000, n_images=200):
     return out
 
 
-def main(which=("kernels", "nets", "configs", "c2")):
+
+
+def deform_cases(n_images=6, seed=5, epoch=2):
+    from convkit import augment
+    out = {}
+    for shp, (c, size) in DEFORM_SHAPES.items():
+        imgs, labels = glyph_images(n_images, 10, size, c, seed=3)
+        x = ck.from_bytes(imgs, labels, 10, "train", F32).images
+        out[f"{shp}_u8"] = imgs
+        for name, kw in DEFORM_CFGS.items():
+            cfg = augment.DeformationConfig(**kw)
+            prm, defd = [], []
+            for i in range(n_images):
+                p = augment.sample_params(cfg, [seed, epoch, i])
+                prm.append([p.translate[0], p.translate[1], p.rotate, p.scale[0], p.scale[1],
+                            p.shear_h, p.elastic_alpha, float(p.seed)])
+                defd.append(augment.deform_channels(x[i], p))
+            out[f"{shp}_{name}_params"] = np.array(prm)
+            out[f"{shp}_{name}_out"] = np.stack(defd).astype(F32)
+    # one deformed online epoch of the tiny net (train_epoch with deformation)
+    spec = ck.parse_architecture(SMALL_NETS["tiny"])
+    net = ck.NetworkState(spec, 4, dtype=F32)
+    imgs, labels = glyph_images(24, 3, 13, 1, seed=9)
+    data = ck.from_bytes(imgs, labels, 3, "train", F32)
+    cfg = ck.TrainConfig(epochs=1, eta0=1e-2, seed=seed,
+                         deformation=augment.DeformationConfig(**DEFORM_CFGS["all"]))
+    from convkit import training
+    out["epoch_u8"] = imgs
+    out["epoch_labels"] = labels
+    out["epoch_loss"] = np.array(training.train_epoch(net, data, cfg, 1))
+    out["epoch_params"] = flat_params(net)
+    return out
+
+
+def main(which=("kernels", "nets", "configs", "c2", "deform")):
     kernels.set_workers(1)
     if "kernels" in which:
         np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernel_cases())
@@ -296,7 +336,10 @@ def main(which=("kernels", "nets", "configs", "c2")):
     if "c2" in which:
         np.savez_compressed(os.path.join(HERE, "c2_traj.npz"), **c2_trajectory())
         print("c2_traj.npz written")
+    if "deform" in which:
+        np.savez_compressed(os.path.join(HERE, "deform.npz"), **deform_cases())
+        print("deform.npz written")
 
 
 if __name__ == "__main__":
-    main(tuple(sys.argv[1:]) or ("kernels", "nets", "configs", "c2"))
+    main(tuple(sys.argv[1:]) or ("kernels", "nets", "configs", "c2", "deform"))
