@@ -41,7 +41,7 @@ class DeviceDataset:
             self.labels = pinned["labels"].to(dev, non_blocking=True)
             return
         if data.raw is not None:
-            self.images = torch.from_numpy(np.ascontiguousarray(data.raw)).to(dev)
+            self.images = torch.from_numpy(np.require(data.raw, requirements=["C", "W"])).to(dev)
             self.lut = torch.from_numpy(byte_lut()).to(dev)
         else:   # arbitrary float32 inputs: the engine reads them directly
             self.images = torch.from_numpy(
