@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_1102_0183_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libckb200.so")
-SOURCES = ["ck_seam.cu", "ck_net.cu", "ck_deform.cu"]
+SOURCES = ["ck_seam.cu", "ck_net.cu", "ck_deform.cu", "ck_tc.cu"]
 HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_kernels.cuh", "ck_host.h", "ck_specs.inc"]
 
 COMPILE_FLAGS = [

@@ -266,6 +266,28 @@ int ck_deform_apply(const uint8_t* images, const float* lut, int channels, int h
                     int width, int64_t n, const ck_deform_params* params,
                     const double* gauss_w, int radius, float* out, ck_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * 4. Tensor-core batched evaluation (training.evaluate / predict at
+ *    throughput, within a stated tolerance — NOT bit-exact; ck_net_eval is
+ *    the bit-exact path).  Every conv / contrast / FC layer is an implicit
+ *    GEMM on tcgen05 (fp16 operands, f32 accumulation in TMEM); passes = 3
+ *    splits operands into fp16 hi+lo (Ah*Bh + Ah*Bl + Al*Bh, ~f32 accurate),
+ *    passes = 1 is plain fp16.  The plan is built from the same layer
+ *    descriptions as ck_net_create and owns activation buffers for
+ *    max_batch images; ck_tc_set_params converts a parameter vector in
+ *    NetworkState.parameters() order (DEVICE pointer, e.g.
+ *    ck_net_device_params) into its weight matrices.
+ * ---------------------------------------------------------------------- */
+typedef struct ck_tc_eval ck_tc_eval;
+int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t max_batch,
+                 int passes, ck_tc_eval** out);
+int ck_tc_destroy(ck_tc_eval* plan);
+int ck_tc_set_params(ck_tc_eval* plan, const float* params, ck_stream_t stream);
+int ck_tc_eval_run(ck_tc_eval* plan, const uint8_t* images, const float* lut, int64_t first,
+                   int64_t n, int32_t* pred, float* outputs, ck_stream_t stream);
+/* Device pointer of a net's parameter vector (valid until ck_net_destroy). */
+int ck_net_device_params(const ck_net* net, const float** params);
+
 #ifdef __cplusplus
 }
 #endif

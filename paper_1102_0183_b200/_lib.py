@@ -91,6 +91,11 @@ _SIGNATURES = {
     "ck_net_kernel_info": (_i32, [_vp, C.c_char_p, _i32]),
     "ck_deform_epoch": (_i32, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _i32,
                                C.c_uint64, C.c_uint64, _vp, _vp, _vp]),
+    "ck_tc_create": (_i32, [C.POINTER(LayerDesc), _i32, _i32, _i64, _i32, C.POINTER(_vp)]),
+    "ck_tc_destroy": (_i32, [_vp]),
+    "ck_tc_set_params": (_i32, [_vp, _vp, _vp]),
+    "ck_tc_eval_run": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
+    "ck_net_device_params": (_i32, [_vp, C.POINTER(_vp)]),
     "ck_deform_apply": (_i32, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _i32, _vp, _vp]),
 }
 

@@ -829,6 +829,12 @@ int ck_net_set_params(ck_net* net, const float* host, int64_t n) {
   return CK_OK;
 }
 
+int ck_net_device_params(const ck_net* net, const float** params) {
+  CK_CHECK(net && params, CK_E_CONFIG, "null argument");
+  *params = net->d_params;
+  return CK_OK;
+}
+
 int ck_net_get_params(ck_net* net, float* host, int64_t n) {
   CK_CHECK(net && host, CK_E_CONFIG, "null argument");
   CK_CHECK(n == net->n_params, CK_E_DIMENSION, "parameter count mismatch");

@@ -1,0 +1,703 @@
+// ck_tc.cu — batched test-set evaluation on the 5th-generation tensor cores.
+//
+// The bit-exact evaluation path (ck_net_eval) keeps the reference's
+// sequential f32 conv chains and therefore runs on the SIMT pipes.  This file
+// is the throughput path the north star allows "within a stated tolerance":
+// every convolution, the contrast layer and every fully connected layer is an
+// implicit GEMM on tcgen05 (kind::f16, FP32 accumulation in TMEM):
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]
+//     m = (image, out row, out col)              (M tile: 128 rows)
+//     n = destination map / neuron               (N <= 512, one TMEM column each)
+//     k = (source map, kernel row v, kernel col u)   (K chunks of 64)
+//   A[m, k] = X[image, s, r*ty + v - cy, c*tx + u - cx]   (gathered, clamped
+//             for the contrast layer's replicated border)
+//   B[n, k] = the layer's weight (zero where the connection table has no pair)
+//
+// Precision modes: passes = 1 rounds A and B to fp16 (11-bit significand);
+// passes = 3 splits both into fp16 hi + lo parts and accumulates
+// Ah*Bh + Ah*Bl + Al*Bh (K' = 3K), which is within a few f32 ulps of an f32
+// GEMM.  Neither is bit-exact with the reference's sequential f32 chain, so
+// labels are compared by agreement rate (tests/test_gpu_tc.py).
+//
+// Per CTA (256 threads, persistent over M tiles):
+//   * all threads gather the A chunk (128 x 64 fp16) straight into shared
+//     memory in the UMMA no-swizzle K-major core-matrix layout (8 rows x 16 B
+//     per core matrix; K-adjacent cores 128 B apart, 8-row groups 1 KB apart);
+//   * thread 0 streams the matching B chunk (pre-laid-out in HBM in the same
+//     layout) with one cp.async.bulk (TMA bulk copy) onto an mbarrier;
+//   * thread 0 issues tcgen05.mma (M=128, N<=256 per instruction, K=16) for
+//     the chunk and tcgen05.commit's it onto the buffer's mbarrier, so the
+//     gather of chunk c+1 overlaps the MMAs of chunk c (double buffer);
+//   * epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32*(w%4)..+31),
+//     bias + scaled tanh, store (image, map, row, col) f32.
+// Pooling and the argmax run in small SIMT kernels between the GEMMs.
+#include <cuda_fp16.h>
+#include <math.h>
+
+#include <vector>
+
+#include "ck_host.h"
+
+namespace ck {
+namespace tc {
+
+constexpr int BM = 128;        // rows per tile (TMEM lanes)
+constexpr int BK = 64;         // K per chunk (128 B of fp16 per row)
+constexpr int THREADS = 256;
+constexpr float kActScale = 1.7159f, kActGain = 0.6666f;
+
+struct GemmLayer {
+  int S, H, W;                 // source maps / rows / cols
+  int kx, ky, tx, ty, cx, cy;  // kernel, stride (skip + 1), centre offset (contrast)
+  int N, OH, OW;               // destinations, output rows / cols
+  int K, K_pad, N_pad, passes, parts;    // parts: 2 (hi + lo) when passes == 3
+  int act;                     // 1: 1.7159 tanh(0.6666 a); 0: identity
+  int dst_maps, dst_off;       // output tensor map count and this layer's first map
+  const float* X;              // (B, S, H, W)
+  float* Y;                    // (B, dst_maps, OH, OW)
+  const __half* Bw;            // (K_pad / BK, parts, N_pad * BK) core-matrix layout
+  const float* bias;           // N (nullable)
+  const int* kdec;             // K_pad tap codes (see gemm_kernel), -1 for padding
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;      // descriptor version (sm_100)
+  return d;                    // base offset 0, SWIZZLE_NONE
+}
+
+__device__ __forceinline__ uint32_t instr_desc(int n) {
+  return (1u << 4)                    // D format F32
+         | (0u << 7) | (0u << 10)     // A, B fp16
+         | ((uint32_t)(n >> 3) << 17) // N
+         | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Shared memory: [A stages (hi[, lo]) | B stages (hi[, lo]) | kdec | barriers].
+// One gather per K chunk feeds every pass: with SPLIT the chunk is stored as
+// fp16 hi and lo parts and the MMAs Ah*Bh + Ah*Bl + Al*Bh run back to back.
+// kdec[k]: CLAMP (contrast) s<<16 | v<<8 | u; otherwise the element offset
+// s*H*W + v*W + u of the tap relative to the row's window origin; -1 = pad.
+template <bool CLAMP, bool SPLIT>
+__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M, int tmem_cols,
+                                                          int stages) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int NP = SPLIT ? 2 : 1;                 // operand parts
+  const int a_bytes = BM * BK * 2;                  // one part of one stage
+  const int b_bytes = G.N_pad * BK * 2;
+  uint8_t* As = smem;                               // [stage][part] a_bytes
+  uint8_t* Bs = smem + stages * NP * a_bytes;       // [stage][part] b_bytes (hi then lo)
+  int* kdec = reinterpret_cast<int*>(Bs + stages * NP * b_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kdec + ((G.K_pad + 1) & ~1));
+  uint64_t* load_bar = bars;        // [stages]: B chunk landed
+  uint64_t* mma_bar = bars + 2;     // [stages]: MMAs reading stage s done
+  __shared__ uint32_t tmem_slot;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int k = tid; k < G.K_pad; k += THREADS) kdec[k] = G.kdec[k];
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(bars + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  const int HW = G.H * G.W;
+  const int cells = G.OH * G.OW;
+  const int n_sub = (G.N_pad + 255) / 256;
+  const int chunks = G.K_pad / BK;
+  int64_t g = 0;                          // global chunk counter (stage phases)
+
+  for (int64_t tile = blockIdx.x; tile * BM < M; tile += gridDim.x) {
+    const int row = tid & (BM - 1);
+    const int64_t m = tile * BM + row;
+    const bool valid = m < M;
+    const float* xrow = G.X;
+    int r0 = 0, c0 = 0;
+    if (valid) {
+      const int64_t img = m / cells;
+      const int cell = (int)(m - img * cells);
+      r0 = (cell / G.OW) * G.ty - G.cy;
+      c0 = (cell % G.OW) * G.tx - G.cx;
+      xrow = G.X + img * (int64_t)G.S * HW + (CLAMP ? 0 : r0 * G.W + c0);
+    }
+    for (int ch = 0; ch < chunks; ++ch, ++g) {
+      const int st = stages == 2 ? (int)(g & 1) : 0;
+      const int64_t use = stages == 2 ? (g >> 1) : g;   // uses of this stage so far
+      if (use >= 1) mbar_wait(&mma_bar[st], (unsigned)((use - 1) & 1));
+      uint8_t* a_st = As + st * NP * a_bytes;
+      uint8_t* b_st = Bs + st * NP * b_bytes;
+      if (tid == 0) bulk_load(b_st, G.Bw + (int64_t)ch * NP * G.N_pad * BK, NP * b_bytes, &load_bar[st]);
+      const int kc0 = ch * BK;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int kg = (tid >> 7) + 2 * it;          // 0..7: core matrix along K
+        float x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int dec = kdec[kc0 + kg * 8 + e];
+          x[e] = 0.f;
+          if (valid && dec >= 0) {
+            if (CLAMP) {
+              const int s = dec >> 16, v = (dec >> 8) & 0xFF, u = dec & 0xFF;
+              const int rr = min(max(r0 + v, 0), G.H - 1);
+              const int cc = min(max(c0 + u, 0), G.W - 1);
+              x[e] = __ldg(xrow + (int64_t)s * HW + rr * G.W + cc);
+            } else {
+              x[e] = __ldg(xrow + dec);
+            }
+          }
+        }
+        const int off = (row >> 3) * 1024 + kg * 128 + (row & 7) * 16;
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const __half h0 = __float2half_rn(x[e]), h1 = __float2half_rn(x[e + 1]);
+          hi[e >> 1] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+          if (SPLIT) {
+            const __half l0 = __float2half_rn(x[e] - __half2float(h0));
+            const __half l1 = __float2half_rn(x[e + 1] - __half2float(h1));
+            lo[e >> 1] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+          }
+        }
+        *reinterpret_cast<uint4*>(a_st + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        if (SPLIT) *reinterpret_cast<uint4*>(a_st + a_bytes + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        mbar_wait(&load_bar[st], (unsigned)(use & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ah = smem_u32(a_st), bh = smem_u32(b_st);
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks) {
+          for (int j = 0; j < n_sub; ++j) {
+            const int n0 = j * 256;
+            const uint32_t id = instr_desc(min(256, G.N_pad - n0));
+            const uint32_t boff = (n0 >> 3) * 1024 + ks * 256;
+            const uint64_t a_hi = umma_desc(ah + ks * 256, 128, 1024);
+            const uint64_t b_hi = umma_desc(bh + boff, 128, 1024);
+            mma_f16(tmem + n0, a_hi, b_hi, id, (ch > 0 || ks > 0) ? 1 : 0);
+            if (SPLIT) {
+              mma_f16(tmem + n0, a_hi, umma_desc(bh + b_bytes + boff, 128, 1024), id, 1);
+              mma_f16(tmem + n0, umma_desc(ah + a_bytes + ks * 256, 128, 1024), b_hi, id, 1);
+            }
+          }
+        }
+        mma_commit(&mma_bar[st]);
+      }
+    }
+    // epilogue: wait for the tile's last MMAs
+    {
+      const int64_t gl = g - 1;
+      const int st = stages == 2 ? (int)(gl & 1) : 0;
+      const int64_t use = stages == 2 ? (gl >> 1) : gl;
+      mbar_wait(&mma_bar[st], (unsigned)(use & 1));
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    {
+      const int quarter = warp & 3;
+      const int erow = quarter * 32 + lane;
+      const int64_t em = tile * BM + erow;
+      int64_t obase = 0;
+      if (em < M) {
+        const int64_t img = em / cells;
+        const int cell = (int)(em - img * cells);
+        obase = (img * G.dst_maps + G.dst_off) * (int64_t)cells + cell;
+      }
+      for (int c16 = (warp >> 2); c16 * 16 < G.N_pad; c16 += THREADS / 128) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c16 * 16, v);
+        if (em < M) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int n = c16 * 16 + i;
+            if (n < G.N) {
+              float a = v[i] + (G.bias ? __ldg(G.bias + n) : 0.f);
+              if (G.act) a = kActScale * tanhf(kActGain * a);
+              G.Y[obase + (int64_t)n * cells] = a;
+            }
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+}
+
+// B[n, k] = src[wmap[n * K_pad + k]] (or 0) in the chunked core-matrix
+// layout: per K chunk the hi block, then (parts = 2) the lo block.
+__global__ void fill_weights(const float* __restrict__ src, const int* __restrict__ wmap, int N_pad,
+                             int K_pad, int parts, __half* __restrict__ out) {
+  const int64_t total = (int64_t)parts * N_pad * K_pad;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % K_pad);
+    const int n = (int)((i / K_pad) % N_pad);
+    const int p = (int)(i / ((int64_t)K_pad * N_pad));
+    const int idx = wmap[(int64_t)n * K_pad + k];
+    const float w = idx >= 0 ? src[idx] : 0.f;
+    const __half hi = __float2half_rn(w);
+    const __half h = p == 1 ? __float2half_rn(w - __half2float(hi)) : hi;
+    const int ch = k / BK;
+    const int kk = k % BK;
+    const int64_t off = ((int64_t)ch * parts + p) * N_pad * BK +
+                        ((n >> 3) * 1024 + (kk >> 3) * 128 + (n & 7) * 16 + (kk & 7) * 2) / 2;
+    out[off] = h;
+  }
+}
+
+__global__ void load_input(const uint8_t* __restrict__ images, const float* __restrict__ lut,
+                           int64_t first, int64_t n_vals, int64_t per_img, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_vals;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = first * per_img + i;
+    out[i] = lut ? __ldg(lut + images[src]) : reinterpret_cast<const float*>(images)[src];
+  }
+}
+
+// max-pool, strict '>' (first maximum in row-major scan), trailing cells dropped
+__global__ void pool_kernel(const float* __restrict__ X, int maps_total, int H, int W, int px, int py,
+                            int OH, int OW, float* __restrict__ Y) {
+  const int64_t total = (int64_t)maps_total * OH * OW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % OW);
+    const int r = (int)((i / OW) % OH);
+    const int64_t m = i / ((int64_t)OW * OH);
+    const float* src = X + m * H * W + (int64_t)(r * py) * W + c * px;
+    float best = src[0];
+    for (int v = 0; v < py; ++v)
+      for (int u = 0; u < px; ++u) {
+        const float x = src[v * W + u];
+        if (x > best) best = x;
+      }
+    Y[i] = best;
+  }
+}
+
+// contrast layer originals: maps [0, C) of the output = the input channels
+__global__ void copy_maps(const float* __restrict__ X, int64_t per_img_in, int64_t per_img_out,
+                          int64_t n_img, float* __restrict__ Y) {
+  const int64_t total = n_img * per_img_in;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / per_img_in;
+    Y[b * per_img_out + (i - b * per_img_in)] = X[i];
+  }
+}
+
+__global__ void argmax_kernel(const float* __restrict__ Y, int64_t n, int n_cls, int32_t* pred,
+                              float* outputs) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const float* y = Y + b * n_cls;
+    int best = 0;
+    for (int j = 1; j < n_cls; ++j)
+      if (y[j] > y[best]) best = j;
+    pred[b] = best;
+    if (outputs)
+      for (int j = 0; j < n_cls; ++j) outputs[b * n_cls + j] = y[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host plan
+
+enum StepKind { ST_GEMM = 0, ST_POOL = 1, ST_COPY = 2 };
+
+struct Step {
+  int kind;
+  int layer;
+  GemmLayer g;                  // ST_GEMM (X, Y patched per chunk)
+  int64_t M_per_img;            // GEMM rows per image
+  int tmem_cols;
+  int clamp, stages;
+  size_t smem;
+  int src_buf, dst_buf;         // activation buffer indices
+  // pool / copy
+  int maps, H, W, px, py, OH, OW;
+  int64_t per_in, per_out;
+  // parameter source
+  int64_t param_off;            // offset of the layer's parameters (-1: fixed)
+  int* d_wmap = nullptr;
+  int* d_kdec = nullptr;
+  int* d_bmap = nullptr;
+  __half* d_B = nullptr;
+  float* d_bias = nullptr;
+  float* d_fixed = nullptr;     // contrast coefficients (f32)
+};
+
+}  // namespace tc
+}  // namespace ck
+
+struct ck_tc_eval {
+  int device = 0;
+  int passes = 3;
+  int64_t max_batch = 0;
+  int n_classes = 0;
+  int64_t in_per_img = 0;
+  std::vector<ck::tc::Step> steps;
+  std::vector<float*> bufs;            // activation buffers (max_batch * cells each)
+  std::vector<int64_t> buf_cells;
+  int final_buf = 0;
+  int sms = 148;
+};
+
+namespace ck {
+namespace tc {
+
+static int64_t round_up(int64_t v, int64_t q) { return (v + q - 1) / q * q; }
+
+static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int ky, int tx, int ty,
+                     int cx, int cy, int N, int OH, int OW, int act, int dst_maps, int dst_off,
+                     const std::vector<int>& kdec_host_in, const std::vector<int>& wmap,
+                     const std::vector<int>& bmap) {
+  GemmLayer& g = st.g;
+  g.S = S; g.H = H; g.W = W; g.kx = kx; g.ky = ky; g.tx = tx; g.ty = ty; g.cx = cx; g.cy = cy;
+  g.N = N; g.OH = OH; g.OW = OW; g.act = act; g.dst_maps = dst_maps; g.dst_off = dst_off;
+  g.K = S * kx * ky;
+  g.K_pad = (int)round_up(g.K, BK);
+  g.N_pad = (int)round_up(N, 16);
+  CK_CHECK(g.N_pad <= 512, CK_E_DIMENSION, "tensor-core eval: more than 512 outputs per layer");
+  CK_CHECK(kx < 256 && ky < 256 && S < 32768, CK_E_DIMENSION, "tensor-core eval: kernel too large");
+  g.passes = P->passes;
+  g.parts = g.passes == 3 ? 2 : 1;
+  int cols = 32;
+  while (cols < g.N_pad) cols <<= 1;
+  st.tmem_cols = cols;
+  st.M_per_img = (int64_t)OH * OW;
+  st.clamp = cx > 0 || cy > 0;
+  auto smem_for = [&](int stages) {
+    return (size_t)stages * g.parts * ((size_t)BM * BK * 2 + (size_t)g.N_pad * BK * 2) +
+           (size_t)((g.K_pad + 1) & ~1) * 4 + 4 * 8;
+  };
+  st.stages = smem_for(2) <= 220 * 1024 ? 2 : 1;
+  st.smem = smem_for(st.stages);
+  CK_CHECK(st.smem <= 220 * 1024, CK_E_DIMENSION, "tensor-core eval: tile exceeds shared memory");
+  std::vector<int> kdec(g.K_pad, -1);
+  for (int k = 0; k < g.K; ++k) {
+    const int dec = kdec_host_in[k];
+    kdec[k] = st.clamp ? dec : (dec >> 16) * H * W + ((dec >> 8) & 0xFF) * W + (dec & 0xFF);
+  }
+  std::vector<int> wm((size_t)g.N_pad * g.K_pad, -1);
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < g.K; ++k) wm[(size_t)n * g.K_pad + k] = wmap[(size_t)n * g.K + k];
+  CK_CUDA_TRY(cudaMalloc(&st.d_kdec, sizeof(int) * g.K_pad));
+  CK_CUDA_TRY(cudaMemcpy(st.d_kdec, kdec.data(), sizeof(int) * g.K_pad, cudaMemcpyHostToDevice));
+  CK_CUDA_TRY(cudaMalloc(&st.d_wmap, sizeof(int) * wm.size()));
+  CK_CUDA_TRY(cudaMemcpy(st.d_wmap, wm.data(), sizeof(int) * wm.size(), cudaMemcpyHostToDevice));
+  CK_CUDA_TRY(cudaMalloc(&st.d_B, sizeof(__half) * (size_t)g.parts * g.N_pad * g.K_pad));
+  if (!bmap.empty()) {
+    CK_CUDA_TRY(cudaMalloc(&st.d_bmap, sizeof(int) * N));
+    CK_CUDA_TRY(cudaMemcpy(st.d_bmap, bmap.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+    CK_CUDA_TRY(cudaMalloc(&st.d_bias, sizeof(float) * N));
+  }
+  g.kdec = st.d_kdec;
+  g.Bw = st.d_B;
+  g.bias = st.d_bias;
+  st.kind = ST_GEMM;
+  return CK_OK;
+}
+
+typedef void (*GemmFn)(GemmLayer, int64_t, int, int);
+static GemmFn gemm_fn(bool clamp, bool split) {
+  if (clamp) return split ? gemm_kernel<true, true> : gemm_kernel<true, false>;
+  return split ? gemm_kernel<false, true> : gemm_kernel<false, false>;
+}
+
+__global__ void gather_bias(const float* __restrict__ params, const int* __restrict__ bmap, int n,
+                            float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = params[bmap[i]];
+}
+
+}  // namespace tc
+}  // namespace ck
+
+using ck::tc::Step;
+
+extern "C" {
+
+int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t max_batch,
+                 int passes, ck_tc_eval** out) {
+  CK_CHECK(layers && out && n_layers >= 2, CK_E_CONFIG, "bad arguments");
+  CK_CHECK(passes == 1 || passes == 3, CK_E_CONFIG, "passes must be 1 or 3");
+  CK_CHECK(max_batch >= 1, CK_E_CONFIG, "max_batch must be >= 1");
+  CK_CHECK(layers[0].kind == CK_LAYER_INPUT, CK_E_CONFIG, "first layer must be the input");
+  CK_CUDA_TRY(cudaSetDevice(device));
+  ck_tc_eval* P = new ck_tc_eval();
+  P->device = device;
+  P->passes = passes;
+  P->max_batch = max_batch;
+  CK_CUDA_TRY(cudaDeviceGetAttribute(&P->sms, cudaDevAttrMultiProcessorCount, device));
+  auto fail = [&](int rc) {
+    ck_tc_destroy(P);
+    return rc;
+  };
+  // one activation buffer per layer
+  for (int i = 0; i < n_layers; ++i) {
+    const ck_layer_desc& L = layers[i];
+    const int64_t cells = (int64_t)L.maps * L.width * L.height;
+    float* b = nullptr;
+    if (cudaMalloc(&b, sizeof(float) * cells * max_batch) != cudaSuccess)
+      return fail(ck::set_error(CK_E_NOMEM, "tensor-core eval: activation buffers"));
+    P->bufs.push_back(b);
+    P->buf_cells.push_back(cells);
+  }
+  P->in_per_img = P->buf_cells[0];
+  int64_t poff = 0;   // parameter offset (NetworkState.parameters() order)
+  for (int i = 1; i < n_layers; ++i) {
+    const ck_layer_desc& L = layers[i];
+    const ck_layer_desc& Pv = layers[i - 1];
+    Step st;
+    st.layer = i;
+    st.src_buf = i - 1;
+    st.dst_buf = i;
+    st.param_off = -1;
+    const int S = Pv.maps, H = Pv.height, W = Pv.width;
+    if (L.kind == CK_LAYER_POOL) {
+      st.kind = ck::tc::ST_POOL;
+      st.maps = S; st.H = H; st.W = W; st.px = L.px; st.py = L.py; st.OH = L.height; st.OW = L.width;
+      P->steps.push_back(st);
+      continue;
+    }
+    if (L.kind == CK_LAYER_IMGPROC) {
+      // originals, then one GEMM: dest (f, c) <- filter f on channel c
+      Step cp = st;
+      cp.kind = ck::tc::ST_COPY;
+      cp.per_in = (int64_t)S * H * W;
+      cp.per_out = (int64_t)L.maps * L.height * L.width;
+      P->steps.push_back(cp);
+      const int F = L.n_filters, fh = L.filter_h, fw = L.filter_w;
+      const int N = F * S, K = S * fh * fw;
+      std::vector<int> kdec(K), wmap((size_t)N * K, -1);
+      std::vector<float> coef((size_t)F * fh * fw);
+      for (int j = 0; j < F * fh * fw; ++j) coef[j] = (float)L.filter_coeffs[j];
+      for (int s = 0; s < S; ++s)
+        for (int v = 0; v < fh; ++v)
+          for (int u = 0; u < fw; ++u) kdec[(s * fh + v) * fw + u] = s << 16 | v << 8 | u;
+      for (int f = 0; f < F; ++f)
+        for (int c = 0; c < S; ++c)
+          for (int v = 0; v < fh; ++v)
+            for (int u = 0; u < fw; ++u)
+              wmap[(size_t)(f * S + c) * K + (c * fh + v) * fw + u] = (f * fh + v) * fw + u;
+      int rc = ck::tc::make_gemm(P, st, S, H, W, fw, fh, 1, 1, fw / 2, fh / 2, N, L.height, L.width,
+                                 0, L.maps, S, kdec, wmap, {});
+      if (rc) return fail(rc);
+      if (cudaMalloc(&st.d_fixed, sizeof(float) * coef.size()) != cudaSuccess ||
+          cudaMemcpy(st.d_fixed, coef.data(), sizeof(float) * coef.size(),
+                     cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail(ck::set_error(CK_E_NOMEM, "tensor-core eval: filter coefficients"));
+      P->steps.push_back(st);
+      continue;
+    }
+    if (L.kind == CK_LAYER_CONV) {
+      const int kx = L.kx, ky = L.ky, N = L.maps, K = S * kx * ky;
+      std::vector<int> kdec(K), wmap((size_t)N * K, -1), bmap(N);
+      for (int s = 0; s < S; ++s)
+        for (int v = 0; v < ky; ++v)
+          for (int u = 0; u < kx; ++u) kdec[(s * ky + v) * kx + u] = s << 16 | v << 8 | u;
+      for (int d = 0; d < N; ++d) {
+        for (int64_t p = L.fwd_offsets[d]; p < L.fwd_offsets[d + 1]; ++p) {
+          const int s = (int)L.fwd_srcs[p];
+          for (int v = 0; v < ky; ++v)
+            for (int u = 0; u < kx; ++u)
+              wmap[(size_t)d * K + (s * ky + v) * kx + u] =
+                  (int)(poff + L.fwd_widx[p] + v * kx + u);
+        }
+        bmap[d] = (int)(poff + L.bias_offset[d]);
+      }
+      int rc = ck::tc::make_gemm(P, st, S, H, W, kx, ky, L.sx + 1, L.sy + 1, 0, 0, N, L.height,
+                                 L.width, 1, N, 0, kdec, wmap, bmap);
+      if (rc) return fail(rc);
+      st.param_off = poff;
+      poff += L.arena_size;
+      P->steps.push_back(st);
+      continue;
+    }
+    if (L.kind == CK_LAYER_FC) {
+      const int n_in = S * H * W, N = L.maps;
+      std::vector<int> kdec(n_in), wmap((size_t)N * n_in), bmap(N);
+      for (int s = 0; s < S; ++s)
+        for (int v = 0; v < H; ++v)
+          for (int u = 0; u < W; ++u) kdec[(s * H + v) * W + u] = s << 16 | v << 8 | u;
+      for (int o = 0; o < N; ++o) {
+        for (int k = 0; k < n_in; ++k) wmap[(size_t)o * n_in + k] = (int)(poff + (int64_t)k * N + o);
+        bmap[o] = (int)(poff + (int64_t)n_in * N + o);
+      }
+      int rc = ck::tc::make_gemm(P, st, S, H, W, W, H, 1, 1, 0, 0, N, 1, 1, 1, N, 0, kdec, wmap,
+                                 bmap);
+      if (rc) return fail(rc);
+      st.param_off = poff;
+      poff += (int64_t)n_in * N + N;
+      P->steps.push_back(st);
+      continue;
+    }
+    return fail(ck::set_error(CK_E_CONFIG, "tensor-core eval: unsupported layer kind"));
+  }
+  CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG, "last layer must be the output");
+  P->n_classes = layers[n_layers - 1].maps;
+  P->final_buf = n_layers - 1;
+  // the fixed (contrast) weights once
+  for (auto& st : P->steps)
+    if (st.kind == ck::tc::ST_GEMM && st.d_fixed) {
+      ck::tc::fill_weights<<<256, 256>>>(st.d_fixed, st.d_wmap, st.g.N_pad, st.g.K_pad,
+                                         st.g.parts, st.d_B);
+      ck::count_launch();
+    }
+  CK_CUDA_TRY(cudaDeviceSynchronize());
+  *out = P;
+  return CK_OK;
+}
+
+int ck_tc_destroy(ck_tc_eval* P) {
+  if (!P) return CK_OK;
+  cudaSetDevice(P->device);
+  for (float* b : P->bufs) cudaFree(b);
+  for (auto& st : P->steps) {
+    cudaFree(st.d_wmap);
+    cudaFree(st.d_kdec);
+    cudaFree(st.d_bmap);
+    cudaFree(st.d_B);
+    cudaFree(st.d_bias);
+    cudaFree(st.d_fixed);
+  }
+  delete P;
+  return CK_OK;
+}
+
+int ck_tc_set_params(ck_tc_eval* P, const float* params, ck_stream_t stream) {
+  CK_CHECK(P && params, CK_E_CONFIG, "null argument");
+  CK_CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  for (auto& st : P->steps) {
+    if (st.kind != ck::tc::ST_GEMM || st.param_off < 0) continue;
+    ck::tc::fill_weights<<<P->sms * 4, 256, 0, s>>>(params, st.d_wmap, st.g.N_pad, st.g.K_pad,
+                                                     st.g.parts, st.d_B);
+    ck::tc::gather_bias<<<(st.g.N + 255) / 256, 256, 0, s>>>(params, st.d_bmap, st.g.N,
+                                                             st.d_bias);
+    ck::count_launch(2);
+  }
+  CK_CUDA_TRY(cudaGetLastError());
+  return CK_OK;
+}
+
+int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64_t first, int64_t n,
+                   int32_t* pred, float* outputs, ck_stream_t stream) {
+  CK_CHECK(P && images && pred, CK_E_CONFIG, "null argument");
+  CK_CUDA_TRY(cudaSetDevice(P->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  for (auto& st : P->steps)
+    if (st.kind == ck::tc::ST_GEMM)
+      CK_CUDA_TRY(cudaFuncSetAttribute(ck::tc::gemm_fn(st.clamp, st.g.parts == 2),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  for (int64_t b0 = 0; b0 < n; b0 += P->max_batch) {
+    const int64_t nb = std::min(P->max_batch, n - b0);
+    ck::tc::load_input<<<P->sms * 4, 256, 0, s>>>(images, lut, first + b0, nb * P->in_per_img,
+                                                  P->in_per_img, P->bufs[0]);
+    ck::count_launch();
+    for (auto& st : P->steps) {
+      const float* X = P->bufs[st.src_buf];
+      float* Y = P->bufs[st.dst_buf];
+      if (st.kind == ck::tc::ST_POOL) {
+        const int64_t total = nb * st.maps * (int64_t)st.OH * st.OW;
+        ck::tc::pool_kernel<<<ck::blocks_for(total, 256), 256, 0, s>>>(
+            X, (int)(nb * st.maps), st.H, st.W, st.px, st.py, st.OH, st.OW, Y);
+      } else if (st.kind == ck::tc::ST_COPY) {
+        ck::tc::copy_maps<<<P->sms * 4, 256, 0, s>>>(X, st.per_in, st.per_out, nb, Y);
+      } else {
+        ck::tc::GemmLayer g = st.g;
+        g.X = X;
+        g.Y = Y;
+        const int64_t M = nb * st.M_per_img;
+        const int64_t tiles = (M + ck::tc::BM - 1) / ck::tc::BM;
+        const int grid = (int)std::min<int64_t>(tiles, P->sms);
+        ck::tc::gemm_fn(st.clamp, st.g.parts == 2)<<<grid, ck::tc::THREADS, st.smem, s>>>(
+            g, M, st.tmem_cols, st.stages);
+      }
+      ck::count_launch();
+    }
+    ck::tc::argmax_kernel<<<ck::blocks_for(nb, 256), 256, 0, s>>>(
+        P->bufs[P->final_buf], nb, P->n_classes, pred + b0,
+        outputs ? outputs + b0 * P->n_classes : nullptr);
+    ck::count_launch();
+  }
+  CK_CUDA_TRY(cudaGetLastError());
+  return CK_OK;
+}
+
+}  // extern "C"

@@ -21,6 +21,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
+from .device import current_stream_handle
 from .errors import ConfigError, DimensionError, PrecisionError, StateError
 from .filters import expand_selection, filter_coefficients
 from .topology import (ConnectionTable, NetworkSpec, build_full_table,
@@ -181,6 +182,8 @@ class NetworkState:
                                          ls.skip if ls.kind == "convolutional" else None,
                                          ls.filters or None))
 
+        self._descs, self._desc_keep = descs, keep     # reused by the tensor-core eval plan
+        self._tc_plans: dict = {}
         handle = C.c_void_p()
         _lib.call("ck_net_create", descs, len(spec.layers), device, C.byref(handle))
         self._handle = handle
@@ -194,7 +197,25 @@ class NetworkState:
 
     # -- lifecycle -----------------------------------------------------
 
+    def tc_plan(self, passes: int = 3, max_batch: int = 4096):
+        """Tensor-core evaluation plan (ck_tc_create) for this net's geometry,
+        loaded with the current parameters."""
+        key = (passes, max_batch)
+        plan = self._tc_plans.get(key)
+        if plan is None:
+            plan = C.c_void_p()
+            _lib.call("ck_tc_create", self._descs, len(self.spec.layers), self.device,
+                      max_batch, passes, C.byref(plan))
+            self._tc_plans[key] = plan
+        params = C.c_void_p()
+        _lib.call("ck_net_device_params", self.handle, C.byref(params))
+        _lib.call("ck_tc_set_params", plan, params, current_stream_handle(self.device))
+        return plan
+
     def close(self) -> None:
+        for plan in getattr(self, "_tc_plans", {}).values():
+            _lib.call("ck_tc_destroy", plan)
+        self._tc_plans = {}
         if self._handle is not None:
             _lib.call("ck_net_destroy", self._handle)
             self._handle = None
