@@ -54,12 +54,21 @@ struct GemmLayer {
   int K, K_pad, N_pad, passes, parts;    // parts: 2 (hi + lo) when passes == 3
   int act;                     // 1: 1.7159 tanh(0.6666 a); 0: identity
   int dst_maps, dst_off;       // output tensor map count and this layer's first map
+  int px, py, PH, PW;          // fused max-pool (1x1: none); output is (PH, PW)
+  int P, bpt;                  // rows per pool block (px*py), blocks per 128-row tile
   const float* X;              // (B, S, H, W)
   float* Y;                    // (B, dst_maps, OH, OW)
   const __half* Bw;            // (K_pad / BK, parts, N_pad * BK) core-matrix layout
   const float* bias;           // N (nullable)
   const int* kdec;             // K_pad tap codes (see gemm_kernel), -1 for padding
 };
+
+// 1.7159 tanh(0.6666 a) through exp: |error| ~1e-7, a few instructions
+// instead of tanhf's slow path (this path is within tolerance, not exact).
+__device__ __forceinline__ float act_fast(float a) {
+  const float e = __expf(2.f * kActGain * fminf(fmaxf(a, -40.f), 40.f));
+  return kActScale * (1.f - __fdividef(2.f, e + 1.f));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -149,9 +158,11 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
   uint8_t* Bs = smem + stages * NP * a_bytes;       // [stage][part] b_bytes (hi then lo)
   int* kdec = reinterpret_cast<int*>(Bs + stages * NP * b_bytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(kdec + ((G.K_pad + 1) & ~1));
+  float* epi = reinterpret_cast<float*>(bars + 4);   // [2][BM][17] epilogue staging
   uint64_t* load_bar = bars;        // [stages]: B chunk landed
   uint64_t* mma_bar = bars + 2;     // [stages]: MMAs reading stage s done
   __shared__ uint32_t tmem_slot;
+  __shared__ int64_t obase_s[BM];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int k = tid; k < G.K_pad; k += THREADS) kdec[k] = G.kdec[k];
@@ -171,22 +182,28 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
   const uint32_t tmem = tmem_slot;
 
   const int HW = G.H * G.W;
-  const int cells = G.OH * G.OW;
   const int n_sub = (G.N_pad + 255) / 256;
   const int chunks = G.K_pad / BK;
   int64_t g = 0;                          // global chunk counter (stage phases)
 
-  for (int64_t tile = blockIdx.x; tile * BM < M; tile += gridDim.x) {
+  // M counts pool blocks: tile t holds blocks [t*bpt, (t+1)*bpt), P rows
+  // each (row-major inside the block, the pool's scan order); the last
+  // 128 - bpt*P rows of a tile are idle.
+  const int pcells = G.PH * G.PW;
+  for (int64_t tile = blockIdx.x; tile * G.bpt < M; tile += gridDim.x) {
     const int row = tid & (BM - 1);
-    const int64_t m = tile * BM + row;
-    const bool valid = m < M;
+    const int64_t blk = tile * G.bpt + row / G.P;
+    const bool valid = row < G.bpt * G.P && blk < M;
     const float* xrow = G.X;
     int r0 = 0, c0 = 0;
     if (valid) {
-      const int64_t img = m / cells;
-      const int cell = (int)(m - img * cells);
-      r0 = (cell / G.OW) * G.ty - G.cy;
-      c0 = (cell % G.OW) * G.tx - G.cx;
+      const int64_t img = blk / pcells;
+      const int pc = (int)(blk - img * pcells);
+      const int w = row % G.P;
+      const int r = (pc / G.PW) * G.py + w / G.px;
+      const int c = (pc % G.PW) * G.px + w % G.px;
+      r0 = r * G.ty - G.cy;
+      c0 = c * G.tx - G.cx;
       xrow = G.X + img * (int64_t)G.S * HW + (CLAMP ? 0 : r0 * G.W + c0);
     }
     for (int ch = 0; ch < chunks; ++ch, ++g) {
@@ -197,34 +214,39 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
       uint8_t* b_st = Bs + st * NP * b_bytes;
       if (tid == 0) bulk_load(b_st, G.Bw + (int64_t)ch * NP * G.N_pad * BK, NP * b_bytes, &load_bar[st]);
       const int kc0 = ch * BK;
+      // all 32 loads of this thread first (latency overlap), then convert
+      float x[4][8];
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
         const int kg = (tid >> 7) + 2 * it;          // 0..7: core matrix along K
-        float x[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int dec = kdec[kc0 + kg * 8 + e];
-          x[e] = 0.f;
+          x[it][e] = 0.f;
           if (valid && dec >= 0) {
             if (CLAMP) {
               const int s = dec >> 16, v = (dec >> 8) & 0xFF, u = dec & 0xFF;
               const int rr = min(max(r0 + v, 0), G.H - 1);
               const int cc = min(max(c0 + u, 0), G.W - 1);
-              x[e] = __ldg(xrow + (int64_t)s * HW + rr * G.W + cc);
+              x[it][e] = __ldg(xrow + (int64_t)s * HW + rr * G.W + cc);
             } else {
-              x[e] = __ldg(xrow + dec);
+              x[it][e] = __ldg(xrow + dec);
             }
           }
         }
+      }
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int kg = (tid >> 7) + 2 * it;
         const int off = (row >> 3) * 1024 + kg * 128 + (row & 7) * 16;
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
-          const __half h0 = __float2half_rn(x[e]), h1 = __float2half_rn(x[e + 1]);
+          const __half h0 = __float2half_rn(x[it][e]), h1 = __float2half_rn(x[it][e + 1]);
           hi[e >> 1] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
           if (SPLIT) {
-            const __half l0 = __float2half_rn(x[e] - __half2float(h0));
-            const __half l1 = __float2half_rn(x[e + 1] - __half2float(h1));
+            const __half l0 = __float2half_rn(x[it][e] - __half2float(h0));
+            const __half l1 = __float2half_rn(x[it][e + 1] - __half2float(h1));
             lo[e >> 1] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
           }
         }
@@ -263,30 +285,51 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
       mbar_wait(&mma_bar[st], (unsigned)(use & 1));
     }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid < G.bpt) {                // output base of each pool block of the tile
+      const int64_t gb = tile * G.bpt + tid;
+      const int64_t img = gb / pcells;
+      obase_s[tid] = gb < M ? (img * G.dst_maps + G.dst_off) * (int64_t)pcells + (gb - img * pcells)
+                            : -1;
+    }
+    __syncthreads();
     {
-      const int quarter = warp & 3;
-      const int erow = quarter * 32 + lane;
-      const int64_t em = tile * BM + erow;
-      int64_t obase = 0;
-      if (em < M) {
-        const int64_t img = em / cells;
-        const int cell = (int)(em - img * cells);
-        obase = (img * G.dst_maps + G.dst_off) * (int64_t)cells + cell;
-      }
-      for (int c16 = (warp >> 2); c16 * 16 < G.N_pad; c16 += THREADS / 128) {
+      // two warp groups take alternate 16-column chunks; warp w reads TMEM
+      // lanes 32*(w%4)..+31 (its rows).  Activated values go through a
+      // per-group staging tile so the pool max runs across rows.
+      const int quarter = warp & 3, grp = warp >> 2, gtid = tid & 127;
+      float* stage = epi + grp * (BM * 17);
+      for (int c16 = grp; c16 * 16 < G.N_pad; c16 += 2) {
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c16 * 16, v);
-        if (em < M) {
+        const int erow = quarter * 32 + lane;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int n = c16 * 16 + i;
-            if (n < G.N) {
-              float a = v[i] + (G.bias ? __ldg(G.bias + n) : 0.f);
-              if (G.act) a = kActScale * tanhf(kActGain * a);
-              G.Y[obase + (int64_t)n * cells] = a;
+        for (int i = 0; i < 16; ++i) {
+          const int n = min(c16 * 16 + i, G.N - 1);
+          float a = v[i] + (G.bias ? __ldg(G.bias + n) : 0.f);
+          if (G.act) a = act_fast(a);
+          stage[erow * 17 + i] = a;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp));
+        // thread -> (block b, columns i0, i0 + istep, ...): no divisions
+        const int istep = BM / G.bpt;
+        if (gtid < istep * G.bpt) {
+          const int b = gtid % G.bpt;
+          const int64_t ob = obase_s[b];
+          if (ob >= 0) {
+            for (int i = gtid / G.bpt; i < 16; i += istep) {
+              const int n = c16 * 16 + i;
+              if (n >= G.N) break;
+              const float* col = stage + b * G.P * 17 + i;
+              float best = col[0];
+              for (int w = 1; w < G.P; ++w) {
+                const float xv = col[w * 17];
+                if (xv > best) best = xv;
+              }
+              G.Y[ob + (int64_t)n * pcells] = best;
             }
           }
         }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp));
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -377,7 +420,52 @@ __global__ void argmax_kernel(const float* __restrict__ Y, int64_t n, int n_cls,
 // ---------------------------------------------------------------------------
 // host plan
 
-enum StepKind { ST_GEMM = 0, ST_POOL = 1, ST_COPY = 2 };
+// Contrast responses on the SIMT pipes (a GEMM with N = filters x channels
+// would leave the tensor core mostly idle and gather-bound): one CTA per
+// (image, channel), replicated-border window staged in shared memory, each
+// thread a strip of 4 cells with a sliding register window; f32 FMA.
+__global__ void __launch_bounds__(256) contrast_kernel(const float* __restrict__ X, int C, int H, int W,
+                                                       const float* __restrict__ coef, int F, int fh,
+                                                       int fw, float* __restrict__ Y, int out_maps) {
+  extern __shared__ float sm[];
+  const int cy = fh / 2, cx = fw / 2;
+  const int PW = W + fw - 1 + 4, PHh = H + fh - 1;
+  float* win = sm;                       // PHh x PW
+  float* cf = sm + PHh * PW;             // F x fh x fw
+  const int64_t img = blockIdx.x / C;
+  const int c = blockIdx.x % C;
+  const float* src = X + (img * C + c) * (int64_t)H * W;
+  for (int i = threadIdx.x; i < PHh * PW; i += blockDim.x) {
+    const int r = min(max(i / PW - cy, 0), H - 1), q = min(max(i % PW - cx, 0), W - 1);
+    win[i] = src[r * W + q];
+  }
+  for (int i = threadIdx.x; i < F * fh * fw; i += blockDim.x) cf[i] = coef[i];
+  __syncthreads();
+  const int strips = (W + 3) / 4;
+  for (int job = threadIdx.x; job < F * H * strips; job += blockDim.x) {
+    const int f = job / (H * strips);
+    const int r = (job / strips) % H;
+    const int c0 = (job % strips) * 4;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int v = 0; v < fh; ++v) {
+      const float* w = win + (r + v) * PW + c0;
+      const float* k = cf + (f * fh + v) * fw;
+      float x0 = w[0], x1 = w[1], x2 = w[2], x3 = w[3];
+      for (int u = 0; u < fw; ++u) {
+        const float kk = k[u];
+        acc[0] = fmaf(kk, x0, acc[0]);
+        acc[1] = fmaf(kk, x1, acc[1]);
+        acc[2] = fmaf(kk, x2, acc[2]);
+        acc[3] = fmaf(kk, x3, acc[3]);
+        x0 = x1; x1 = x2; x2 = x3; x3 = w[u + 4];
+      }
+    }
+    float* out = Y + ((img * out_maps + C + f * C + c) * (int64_t)H + r) * W;
+    for (int q = 0; q < 4 && c0 + q < W; ++q) out[c0 + q] = acc[q];
+  }
+}
+
+enum StepKind { ST_GEMM = 0, ST_POOL = 1, ST_COPY = 2, ST_CONTRAST = 3 };
 
 struct Step {
   int kind;
@@ -399,6 +487,7 @@ struct Step {
   __half* d_B = nullptr;
   float* d_bias = nullptr;
   float* d_fixed = nullptr;     // contrast coefficients (f32)
+  int F = 0, fh = 0, fw = 0, out_maps = 0;   // contrast
 };
 
 }  // namespace tc
@@ -424,11 +513,14 @@ static int64_t round_up(int64_t v, int64_t q) { return (v + q - 1) / q * q; }
 
 static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int ky, int tx, int ty,
                      int cx, int cy, int N, int OH, int OW, int act, int dst_maps, int dst_off,
-                     const std::vector<int>& kdec_host_in, const std::vector<int>& wmap,
-                     const std::vector<int>& bmap) {
+                     int px, int py, const std::vector<int>& kdec_host_in,
+                     const std::vector<int>& wmap, const std::vector<int>& bmap) {
   GemmLayer& g = st.g;
   g.S = S; g.H = H; g.W = W; g.kx = kx; g.ky = ky; g.tx = tx; g.ty = ty; g.cx = cx; g.cy = cy;
   g.N = N; g.OH = OH; g.OW = OW; g.act = act; g.dst_maps = dst_maps; g.dst_off = dst_off;
+  g.px = px; g.py = py; g.PH = OH / py; g.PW = OW / px; g.P = px * py;
+  CK_CHECK(g.P <= BM, CK_E_DIMENSION, "tensor-core eval: pool region above 128 cells");
+  g.bpt = BM / g.P;
   g.K = S * kx * ky;
   g.K_pad = (int)round_up(g.K, BK);
   g.N_pad = (int)round_up(N, 16);
@@ -439,11 +531,11 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
   int cols = 32;
   while (cols < g.N_pad) cols <<= 1;
   st.tmem_cols = cols;
-  st.M_per_img = (int64_t)OH * OW;
+  st.M_per_img = (int64_t)g.PH * g.PW;   // pool blocks per image
   st.clamp = cx > 0 || cy > 0;
   auto smem_for = [&](int stages) {
     return (size_t)stages * g.parts * ((size_t)BM * BK * 2 + (size_t)g.N_pad * BK * 2) +
-           (size_t)((g.K_pad + 1) & ~1) * 4 + 4 * 8;
+           (size_t)((g.K_pad + 1) & ~1) * 4 + 4 * 8 + 2 * BM * 17 * 4;
   };
   st.stages = smem_for(2) <= 220 * 1024 ? 2 : 1;
   st.smem = smem_for(st.stages);
@@ -508,17 +600,19 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
     ck_tc_destroy(P);
     return rc;
   };
-  // one activation buffer per layer
-  for (int i = 0; i < n_layers; ++i) {
-    const ck_layer_desc& L = layers[i];
-    const int64_t cells = (int64_t)L.maps * L.width * L.height;
-    float* b = nullptr;
-    if (cudaMalloc(&b, sizeof(float) * cells * max_batch) != cudaSuccess)
-      return fail(ck::set_error(CK_E_NOMEM, "tensor-core eval: activation buffers"));
-    P->bufs.push_back(b);
-    P->buf_cells.push_back(cells);
-  }
+  // activation buffers per layer, allocated only for layers that are read
+  // or written (a conv fused with its pool writes the pool's buffer)
+  P->bufs.assign(n_layers, nullptr);
+  for (int i = 0; i < n_layers; ++i)
+    P->buf_cells.push_back((int64_t)layers[i].maps * layers[i].width * layers[i].height);
+  auto need = [&](int i) {
+    if (P->bufs[i]) return CK_OK;
+    if (cudaMalloc(&P->bufs[i], sizeof(float) * P->buf_cells[i] * max_batch) != cudaSuccess)
+      return ck::set_error(CK_E_NOMEM, "tensor-core eval: activation buffers");
+    return CK_OK;
+  };
   P->in_per_img = P->buf_cells[0];
+  if (int rc = need(0)) return fail(rc);
   int64_t poff = 0;   // parameter offset (NetworkState.parameters() order)
   for (int i = 1; i < n_layers; ++i) {
     const ck_layer_desc& L = layers[i];
@@ -529,6 +623,12 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
     st.dst_buf = i;
     st.param_off = -1;
     const int S = Pv.maps, H = Pv.height, W = Pv.width;
+    // a conv followed by a max-pool: the pool runs in the GEMM epilogue
+    const bool fuse = L.kind == CK_LAYER_CONV && i + 1 < n_layers &&
+                      layers[i + 1].kind == CK_LAYER_POOL &&
+                      layers[i + 1].px * layers[i + 1].py <= ck::tc::BM;
+    if (fuse) st.dst_buf = i + 1;
+    if (int rc = need(st.dst_buf)) return fail(rc);
     if (L.kind == CK_LAYER_POOL) {
       st.kind = ck::tc::ST_POOL;
       st.maps = S; st.H = H; st.W = W; st.px = L.px; st.py = L.py; st.OH = L.height; st.OW = L.width;
@@ -536,28 +636,19 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
       continue;
     }
     if (L.kind == CK_LAYER_IMGPROC) {
-      // originals, then one GEMM: dest (f, c) <- filter f on channel c
+      // originals, then the filter responses (SIMT, f32)
       Step cp = st;
       cp.kind = ck::tc::ST_COPY;
       cp.per_in = (int64_t)S * H * W;
       cp.per_out = (int64_t)L.maps * L.height * L.width;
       P->steps.push_back(cp);
-      const int F = L.n_filters, fh = L.filter_h, fw = L.filter_w;
-      const int N = F * S, K = S * fh * fw;
-      std::vector<int> kdec(K), wmap((size_t)N * K, -1);
-      std::vector<float> coef((size_t)F * fh * fw);
-      for (int j = 0; j < F * fh * fw; ++j) coef[j] = (float)L.filter_coeffs[j];
-      for (int s = 0; s < S; ++s)
-        for (int v = 0; v < fh; ++v)
-          for (int u = 0; u < fw; ++u) kdec[(s * fh + v) * fw + u] = s << 16 | v << 8 | u;
-      for (int f = 0; f < F; ++f)
-        for (int c = 0; c < S; ++c)
-          for (int v = 0; v < fh; ++v)
-            for (int u = 0; u < fw; ++u)
-              wmap[(size_t)(f * S + c) * K + (c * fh + v) * fw + u] = (f * fh + v) * fw + u;
-      int rc = ck::tc::make_gemm(P, st, S, H, W, fw, fh, 1, 1, fw / 2, fh / 2, N, L.height, L.width,
-                                 0, L.maps, S, kdec, wmap, {});
-      if (rc) return fail(rc);
+      st.kind = ck::tc::ST_CONTRAST;
+      st.F = L.n_filters; st.fh = L.filter_h; st.fw = L.filter_w; st.out_maps = L.maps;
+      st.maps = S; st.H = H; st.W = W;
+      std::vector<float> coef((size_t)st.F * st.fh * st.fw);
+      for (size_t j = 0; j < coef.size(); ++j) coef[j] = (float)L.filter_coeffs[j];
+      st.smem = sizeof(float) * ((size_t)(H + st.fh - 1) * (W + st.fw - 1 + 4) + coef.size());
+      CK_CHECK(st.smem <= 200 * 1024, CK_E_DIMENSION, "tensor-core eval: contrast window too large");
       if (cudaMalloc(&st.d_fixed, sizeof(float) * coef.size()) != cudaSuccess ||
           cudaMemcpy(st.d_fixed, coef.data(), sizeof(float) * coef.size(),
                      cudaMemcpyHostToDevice) != cudaSuccess)
@@ -581,12 +672,14 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
         }
         bmap[d] = (int)(poff + L.bias_offset[d]);
       }
+      const int px = fuse ? layers[i + 1].px : 1, py = fuse ? layers[i + 1].py : 1;
       int rc = ck::tc::make_gemm(P, st, S, H, W, kx, ky, L.sx + 1, L.sy + 1, 0, 0, N, L.height,
-                                 L.width, 1, N, 0, kdec, wmap, bmap);
+                                 L.width, 1, N, 0, px, py, kdec, wmap, bmap);
       if (rc) return fail(rc);
       st.param_off = poff;
       poff += L.arena_size;
       P->steps.push_back(st);
+      if (fuse) ++i;   // the pool layer is done
       continue;
     }
     if (L.kind == CK_LAYER_FC) {
@@ -599,8 +692,8 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
         for (int k = 0; k < n_in; ++k) wmap[(size_t)o * n_in + k] = (int)(poff + (int64_t)k * N + o);
         bmap[o] = (int)(poff + (int64_t)n_in * N + o);
       }
-      int rc = ck::tc::make_gemm(P, st, S, H, W, W, H, 1, 1, 0, 0, N, 1, 1, 1, N, 0, kdec, wmap,
-                                 bmap);
+      int rc = ck::tc::make_gemm(P, st, S, H, W, W, H, 1, 1, 0, 0, N, 1, 1, 1, N, 0, 1, 1, kdec,
+                                 wmap, bmap);
       if (rc) return fail(rc);
       st.param_off = poff;
       poff += (int64_t)n_in * N + N;
@@ -612,13 +705,6 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
   CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG, "last layer must be the output");
   P->n_classes = layers[n_layers - 1].maps;
   P->final_buf = n_layers - 1;
-  // the fixed (contrast) weights once
-  for (auto& st : P->steps)
-    if (st.kind == ck::tc::ST_GEMM && st.d_fixed) {
-      ck::tc::fill_weights<<<256, 256>>>(st.d_fixed, st.d_wmap, st.g.N_pad, st.g.K_pad,
-                                         st.g.parts, st.d_B);
-      ck::count_launch();
-    }
   CK_CUDA_TRY(cudaDeviceSynchronize());
   *out = P;
   return CK_OK;
@@ -661,10 +747,14 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
   CK_CHECK(P && images && pred, CK_E_CONFIG, "null argument");
   CK_CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
-  for (auto& st : P->steps)
+  for (auto& st : P->steps) {
     if (st.kind == ck::tc::ST_GEMM)
       CK_CUDA_TRY(cudaFuncSetAttribute(ck::tc::gemm_fn(st.clamp, st.g.parts == 2),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    if (st.kind == ck::tc::ST_CONTRAST)
+      CK_CUDA_TRY(cudaFuncSetAttribute(ck::tc::contrast_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  }
   for (int64_t b0 = 0; b0 < n; b0 += P->max_batch) {
     const int64_t nb = std::min(P->max_batch, n - b0);
     ck::tc::load_input<<<P->sms * 4, 256, 0, s>>>(images, lut, first + b0, nb * P->in_per_img,
@@ -677,6 +767,9 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
         const int64_t total = nb * st.maps * (int64_t)st.OH * st.OW;
         ck::tc::pool_kernel<<<ck::blocks_for(total, 256), 256, 0, s>>>(
             X, (int)(nb * st.maps), st.H, st.W, st.px, st.py, st.OH, st.OW, Y);
+      } else if (st.kind == ck::tc::ST_CONTRAST) {
+        ck::tc::contrast_kernel<<<(int)(nb * st.maps), 256, st.smem, s>>>(
+            X, st.maps, st.H, st.W, st.d_fixed, st.F, st.fh, st.fw, Y, st.out_maps);
       } else if (st.kind == ck::tc::ST_COPY) {
         ck::tc::copy_maps<<<P->sms * 4, 256, 0, s>>>(X, st.per_in, st.per_out, nb, Y);
       } else {
@@ -684,7 +777,7 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
         g.X = X;
         g.Y = Y;
         const int64_t M = nb * st.M_per_img;
-        const int64_t tiles = (M + ck::tc::BM - 1) / ck::tc::BM;
+        const int64_t tiles = (M + g.bpt - 1) / g.bpt;
         const int grid = (int)std::min<int64_t>(tiles, P->sms);
         ck::tc::gemm_fn(st.clamp, st.g.parts == 2)<<<grid, ck::tc::THREADS, st.smem, s>>>(
             g, M, st.tmem_cols, st.stages);
