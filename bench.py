@@ -319,9 +319,9 @@ def run_ours(args):
     else:
         eval_net = net
 
-    def eval_step():
+    def eval_step(engine="exact"):
         if mine:
-            training.eval_range_async(eval_net, tdd, first, mine, pred, stream=sh)
+            training.eval_range_async(eval_net, tdd, first, mine, pred, stream=sh, engine=engine)
         wrong = (pred[:mine] != labels[first:first + mine]).sum().to(torch.int64).reshape(1)
         if use_dist:
             dist.all_gather_into_tensor(gathered, pred)
@@ -346,6 +346,44 @@ def run_ours(args):
     ev_total = max_over_ranks(sum(ev_ms))
     eval_rate = TEST_IMAGES * args.steps / (ev_total / 1e3)
     err_pct = 100.0 * int(wrong.item()) / TEST_IMAGES
+    exact_labels = gathered.clone()
+
+    # -- the same sharded evaluation on the tensor cores (tcgen05 implicit
+    # GEMM, fp16 hi/lo split, within tolerance) ---------------------------
+    for _ in range(max(3, args.warmup)):
+        eval_step("tc")
+    barrier()
+    tc_ms = []
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        wrong_tc = eval_step("tc")
+        e.record(stream)
+        e.synchronize()
+        tc_ms.append(s.elapsed_time(e))
+    barrier()
+    tc_total = max_over_ranks(sum(tc_ms))
+    tc_rate = TEST_IMAGES * args.steps / (tc_total / 1e3)
+    agree = float((gathered[:TEST_IMAGES] == exact_labels[:TEST_IMAGES]).float().mean().item())
+    peaks = {}
+    ppath = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(ppath):
+        with open(ppath) as f:
+            peaks = json.load(f)
+    tc_peak = peaks.get("bf16_tflops", 2250.0)
+    tc_achieved = work["forward"] * tc_rate / 1e12
+    eval_tc = {"value": tc_rate, "unit": UNIT, "test_images": TEST_IMAGES, "scaling": "strong",
+               "error_pct": 100.0 * int(wrong_tc.item()) / TEST_IMAGES,
+               "label_agreement_with_exact": agree, "ms_per_pass": tc_total / args.steps,
+               "engine": "tcgen05 implicit GEMM, fp16 hi/lo split (3 MMAs), f32 accumulate",
+               "roofline": {"bound": "tensor", "achieved": tc_achieved, "peak": tc_peak,
+                            "unit": "TFLOP/s", "frac": tc_achieved / tc_peak,
+                            "peak_basis": "dense 16-bit tensor peak, MEASURED_PEAKS.json "
+                                          "bf16_tflops" if "bf16_tflops" in peaks else
+                                          "nominal 2.25 PFLOP/s dense 16-bit",
+                            "work": "useful forward FLOPs per image (2 per MAC of the "
+                                    "reference's sparse tables)"}}
 
     # -- end to end through the public API from pinned host bytes ----------
     e2e = None
@@ -499,6 +537,7 @@ def run_ours(args):
                      "collectives": "nccl all_gather(labels) + all_reduce(errors)"
                      if use_dist else "none (single process)",
                      "eval_mflop_per_img": work["forward"] / 1e6},
+            "eval_tc": eval_tc,
             "e2e": e2e,
             "committee": committee,
             "deform": deform,
