@@ -35,6 +35,9 @@
 #include <cuda_fp16.h>
 #include <math.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <vector>
 
 #include "ck_host.h"
@@ -56,6 +59,7 @@ struct GemmLayer {
   int dst_maps, dst_off;       // output tensor map count and this layer's first map
   int px, py, PH, PW;          // fused max-pool (1x1: none); output is (PH, PW)
   int P, bpt;                  // rows per pool block (px*py), blocks per 128-row tile
+  int Nt, n_tiles;             // columns per CTA tile (<= 256), column tiles
   const float* X;              // (B, S, H, W)
   float* Y;                    // (B, dst_maps, OH, OW)
   const __half* Bw;            // (K_pad / BK, parts, N_pad * BK) core-matrix layout
@@ -68,6 +72,14 @@ struct GemmLayer {
 __device__ __forceinline__ float act_fast(float a) {
   const float e = __expf(2.f * kActGain * fminf(fmaxf(a, -40.f), 40.f));
   return kActScale * (1.f - __fdividef(2.f, e + 1.f));
+}
+
+// named barrier of one 128-thread warp group; immediate ids, so the kernel
+// reserves 3 hardware barriers (a register id would reserve all 16 and cap
+// residency at one CTA per SM)
+__device__ __forceinline__ void group_sync(int grp) {
+  if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+  else asm volatile("bar.sync 2, 128;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -113,6 +125,19 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
       : "memory");
 }
 
+__device__ __forceinline__ void expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                         int acc) {
   asm volatile(
@@ -148,12 +173,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // kdec[k]: CLAMP (contrast) s<<16 | v<<8 | u; otherwise the element offset
 // s*H*W + v*W + u of the tap relative to the row's window origin; -1 = pad.
 template <bool CLAMP, bool SPLIT>
-__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M, int tmem_cols,
+__global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M, int tmem_cols,
                                                           int stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NP = SPLIT ? 2 : 1;                 // operand parts
   const int a_bytes = BM * BK * 2;                  // one part of one stage
-  const int b_bytes = G.N_pad * BK * 2;
+  const int b_bytes = G.Nt * BK * 2;                // one part of one stage (a column tile)
   uint8_t* As = smem;                               // [stage][part] a_bytes
   uint8_t* Bs = smem + stages * NP * a_bytes;       // [stage][part] b_bytes (hi then lo)
   int* kdec = reinterpret_cast<int*>(Bs + stages * NP * b_bytes);
@@ -182,7 +207,6 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
   const uint32_t tmem = tmem_slot;
 
   const int HW = G.H * G.W;
-  const int n_sub = (G.N_pad + 255) / 256;
   const int chunks = G.K_pad / BK;
   int64_t g = 0;                          // global chunk counter (stage phases)
 
@@ -190,7 +214,11 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
   // each (row-major inside the block, the pool's scan order); the last
   // 128 - bpt*P rows of a tile are idle.
   const int pcells = G.PH * G.PW;
-  for (int64_t tile = blockIdx.x; tile * G.bpt < M; tile += gridDim.x) {
+  const int64_t m_tiles = (M + G.bpt - 1) / G.bpt;
+  for (int64_t lt = blockIdx.x; lt < m_tiles * G.n_tiles; lt += gridDim.x) {
+    const int64_t tile = lt / G.n_tiles;           // row tile
+    const int n0 = (int)(lt - tile * G.n_tiles) * G.Nt;   // first column of the column tile
+    const int nw = min(G.Nt, G.N_pad - n0);
     const int row = tid & (BM - 1);
     const int64_t blk = tile * G.bpt + row / G.P;
     const bool valid = row < G.bpt * G.P && blk < M;
@@ -212,7 +240,12 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
       if (use >= 1) mbar_wait(&mma_bar[st], (unsigned)((use - 1) & 1));
       uint8_t* a_st = As + st * NP * a_bytes;
       uint8_t* b_st = Bs + st * NP * b_bytes;
-      if (tid == 0) bulk_load(b_st, G.Bw + (int64_t)ch * NP * G.N_pad * BK, NP * b_bytes, &load_bar[st]);
+      if (tid == 0) {
+        const __half* bsrc = G.Bw + (int64_t)ch * NP * G.N_pad * BK + (int64_t)n0 * BK;
+        expect_tx(&load_bar[st], NP * nw * BK * 2);
+        bulk_copy(b_st, bsrc, nw * BK * 2, &load_bar[st]);
+        if (SPLIT) bulk_copy(b_st + b_bytes, bsrc + (int64_t)G.N_pad * BK, nw * BK * 2, &load_bar[st]);
+      }
       const int kc0 = ch * BK;
       // all 32 loads of this thread first (latency overlap), then convert
       float x[4][8];
@@ -261,17 +294,14 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
         const uint32_t ah = smem_u32(a_st), bh = smem_u32(b_st);
 #pragma unroll
         for (int ks = 0; ks < BK / 16; ++ks) {
-          for (int j = 0; j < n_sub; ++j) {
-            const int n0 = j * 256;
-            const uint32_t id = instr_desc(min(256, G.N_pad - n0));
-            const uint32_t boff = (n0 >> 3) * 1024 + ks * 256;
-            const uint64_t a_hi = umma_desc(ah + ks * 256, 128, 1024);
-            const uint64_t b_hi = umma_desc(bh + boff, 128, 1024);
-            mma_f16(tmem + n0, a_hi, b_hi, id, (ch > 0 || ks > 0) ? 1 : 0);
-            if (SPLIT) {
-              mma_f16(tmem + n0, a_hi, umma_desc(bh + b_bytes + boff, 128, 1024), id, 1);
-              mma_f16(tmem + n0, umma_desc(ah + a_bytes + ks * 256, 128, 1024), b_hi, id, 1);
-            }
+          const uint32_t id = instr_desc(nw);
+          const uint32_t boff = ks * 256;
+          const uint64_t a_hi = umma_desc(ah + ks * 256, 128, 1024);
+          const uint64_t b_hi = umma_desc(bh + boff, 128, 1024);
+          mma_f16(tmem, a_hi, b_hi, id, (ch > 0 || ks > 0) ? 1 : 0);
+          if (SPLIT) {
+            mma_f16(tmem, a_hi, umma_desc(bh + b_bytes + boff, 128, 1024), id, 1);
+            mma_f16(tmem, umma_desc(ah + a_bytes + ks * 256, 128, 1024), b_hi, id, 1);
           }
         }
         mma_commit(&mma_bar[st]);
@@ -298,18 +328,18 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
       // per-group staging tile so the pool max runs across rows.
       const int quarter = warp & 3, grp = warp >> 2, gtid = tid & 127;
       float* stage = epi + grp * (BM * 17);
-      for (int c16 = grp; c16 * 16 < G.N_pad; c16 += 2) {
+      for (int c16 = grp; c16 * 16 < nw; c16 += 2) {
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c16 * 16, v);
         const int erow = quarter * 32 + lane;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int n = min(c16 * 16 + i, G.N - 1);
+          const int n = min(n0 + c16 * 16 + i, G.N - 1);
           float a = v[i] + (G.bias ? __ldg(G.bias + n) : 0.f);
           if (G.act) a = act_fast(a);
           stage[erow * 17 + i] = a;
         }
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp));
+        group_sync(grp);
         // thread -> (block b, columns i0, i0 + istep, ...): no divisions
         const int istep = BM / G.bpt;
         if (gtid < istep * G.bpt) {
@@ -317,7 +347,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
           const int64_t ob = obase_s[b];
           if (ob >= 0) {
             for (int i = gtid / G.bpt; i < 16; i += istep) {
-              const int n = c16 * 16 + i;
+              const int n = n0 + c16 * 16 + i;
               if (n >= G.N) break;
               const float* col = stage + b * G.P * 17 + i;
               float best = col[0];
@@ -329,7 +359,7 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(GemmLayer G, int64_t M
             }
           }
         }
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp));
+        group_sync(grp);
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -473,7 +503,7 @@ struct Step {
   GemmLayer g;                  // ST_GEMM (X, Y patched per chunk)
   int64_t M_per_img;            // GEMM rows per image
   int tmem_cols;
-  int clamp, stages;
+  int clamp, stages, ctas_per_sm;
   size_t smem;
   int src_buf, dst_buf;         // activation buffer indices
   // pool / copy
@@ -528,17 +558,30 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
   CK_CHECK(kx < 256 && ky < 256 && S < 32768, CK_E_DIMENSION, "tensor-core eval: kernel too large");
   g.passes = P->passes;
   g.parts = g.passes == 3 ? 2 : 1;
+  // column tiles of <= 256 (one MMA per K step; TMEM <= 256 columns, so
+  // two CTAs fit an SM's 512 columns)
+  g.n_tiles = (g.N_pad + 255) / 256;
+  g.Nt = (int)round_up((g.N_pad + g.n_tiles - 1) / g.n_tiles, 16);
   int cols = 32;
-  while (cols < g.N_pad) cols <<= 1;
+  while (cols < g.Nt) cols <<= 1;
   st.tmem_cols = cols;
   st.M_per_img = (int64_t)g.PH * g.PW;   // pool blocks per image
   st.clamp = cx > 0 || cy > 0;
   auto smem_for = [&](int stages) {
-    return (size_t)stages * g.parts * ((size_t)BM * BK * 2 + (size_t)g.N_pad * BK * 2) +
+    return (size_t)stages * g.parts * ((size_t)BM * BK * 2 + (size_t)g.Nt * BK * 2) +
            (size_t)((g.K_pad + 1) & ~1) * 4 + 4 * 8 + 2 * BM * 17 * 4;
   };
-  st.stages = smem_for(2) <= 220 * 1024 ? 2 : 1;
+  // CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and
+  // TMEM (512 columns per SM) bound it.  Several resident CTAs overlap one
+  // CTA's epilogue with another's gather and MMAs, so a single-stage ring
+  // that fits two CTAs beats a double-buffered one that fits only one.
+  auto occ = [&](size_t sm) {
+    const int by_smem = sm <= 220 * 1024 ? (int)((228 * 1024) / (sm + 1024)) : 0;
+    return std::min(by_smem, 512 / cols);
+  };
+  st.stages = occ(smem_for(2)) >= std::max(1, occ(smem_for(1))) ? 2 : 1;
   st.smem = smem_for(st.stages);
+  st.ctas_per_sm = std::max(1, occ(st.smem));
   CK_CHECK(st.smem <= 220 * 1024, CK_E_DIMENSION, "tensor-core eval: tile exceeds shared memory");
   std::vector<int> kdec(g.K_pad, -1);
   for (int k = 0; k < g.K; ++k) {
@@ -703,6 +746,15 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
     return fail(ck::set_error(CK_E_CONFIG, "tensor-core eval: unsupported layer kind"));
   }
   CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG, "last layer must be the output");
+  for (auto& st : P->steps) {
+    if (st.kind == ck::tc::ST_GEMM)
+      if (cudaSuccess != cudaFuncSetAttribute(ck::tc::gemm_fn(st.clamp, st.g.parts == 2),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) return fail(ck::set_error(CK_E_CUDA, "tensor-core eval: kernel attributes"));
+    if (st.kind == ck::tc::ST_CONTRAST)
+      if (cudaSuccess != cudaFuncSetAttribute(ck::tc::contrast_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) return fail(ck::set_error(CK_E_CUDA, "tensor-core eval: kernel attributes"));
+  }
+
   P->n_classes = layers[n_layers - 1].maps;
   P->final_buf = n_layers - 1;
   CK_CUDA_TRY(cudaDeviceSynchronize());
@@ -747,14 +799,6 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
   CK_CHECK(P && images && pred, CK_E_CONFIG, "null argument");
   CK_CUDA_TRY(cudaSetDevice(P->device));
   cudaStream_t s = (cudaStream_t)stream;
-  for (auto& st : P->steps) {
-    if (st.kind == ck::tc::ST_GEMM)
-      CK_CUDA_TRY(cudaFuncSetAttribute(ck::tc::gemm_fn(st.clamp, st.g.parts == 2),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    if (st.kind == ck::tc::ST_CONTRAST)
-      CK_CUDA_TRY(cudaFuncSetAttribute(ck::tc::contrast_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  }
   for (int64_t b0 = 0; b0 < n; b0 += P->max_batch) {
     const int64_t nb = std::min(P->max_batch, n - b0);
     ck::tc::load_input<<<P->sms * 4, 256, 0, s>>>(images, lut, first + b0, nb * P->in_per_img,
@@ -777,8 +821,8 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
         g.X = X;
         g.Y = Y;
         const int64_t M = nb * st.M_per_img;
-        const int64_t tiles = (M + g.bpt - 1) / g.bpt;
-        const int grid = (int)std::min<int64_t>(tiles, P->sms);
+        const int64_t tiles = (M + g.bpt - 1) / g.bpt * g.n_tiles;
+        const int grid = (int)std::min<int64_t>(tiles, (int64_t)P->sms * st.ctas_per_sm);
         ck::tc::gemm_fn(st.clamp, st.g.parts == 2)<<<grid, ck::tc::THREADS, st.smem, s>>>(
             g, M, st.tmem_cols, st.stages);
       }

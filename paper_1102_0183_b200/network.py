@@ -184,6 +184,8 @@ class NetworkState:
 
         self._descs, self._desc_keep = descs, keep     # reused by the tensor-core eval plan
         self._tc_plans: dict = {}
+        self._tc_loaded: dict = {}     # plan key -> self._version its weights reflect
+        self._version = 0
         handle = C.c_void_p()
         _lib.call("ck_net_create", descs, len(spec.layers), device, C.byref(handle))
         self._handle = handle
@@ -207,9 +209,13 @@ class NetworkState:
             _lib.call("ck_tc_create", self._descs, len(self.spec.layers), self.device,
                       max_batch, passes, C.byref(plan))
             self._tc_plans[key] = plan
-        params = C.c_void_p()
-        _lib.call("ck_net_device_params", self.handle, C.byref(params))
-        _lib.call("ck_tc_set_params", plan, params, current_stream_handle(self.device))
+        if self._tc_loaded.get(key) != self._version:
+            if self._handle is None:
+                raise StateError("network has been closed")
+            params = C.c_void_p()
+            _lib.call("ck_net_device_params", self._handle, C.byref(params))
+            _lib.call("ck_tc_set_params", plan, params, current_stream_handle(self.device))
+            self._tc_loaded[key] = self._version
         return plan
 
     def close(self) -> None:
@@ -228,8 +234,11 @@ class NetworkState:
 
     @property
     def handle(self):
+        """The ck_net handle.  Every use may change the parameters on the
+        device, so it also invalidates the tensor-core plans' weight copies."""
         if self._handle is None:
             raise StateError("network has been closed")
+        self._version += 1
         return self._handle
 
     def set_team(self, kind: int, ctas: int, threads: int = 512) -> None:

@@ -28,7 +28,7 @@ for cfg in sys.argv[1:] or ["C1", "C2", "C3", "C4"]:
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        reps = 5
+        reps = 20
         for _ in range(reps):
             training.eval_range_async(net, dd, 0, N, pred, engine=eng, passes=passes)
         e.record()
