@@ -238,6 +238,13 @@ __device__ __forceinline__ Span cta_span(int64_t n, const TeamCtx& tm) {
   return Span{(int)(un * r / sz), (int)(un * (r + 1) / sz)};
 }
 
+// span of n items over the team ranks [r0, r1) (empty for ranks outside)
+__device__ __forceinline__ Span sub_span(int64_t n, int r0, int r1, const TeamCtx& tm) {
+  if (tm.rank < r0 || tm.rank >= r1) return Span{0, 0};
+  const unsigned un = (unsigned)n, r = (unsigned)(tm.rank - r0), sz = (unsigned)(r1 - r0);
+  return Span{(int)(un * r / sz), (int)(un * (r + 1) / sz)};
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -1207,9 +1214,16 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   const int split = L.wg_split;
   CK_SUBT(tm, 10);
 
+  // The pull (below) is the long pole of this phase: with few source maps
+  // (one per CTA) those CTAs take no weight-gradient work, which the other
+  // ranks share.  Every sum keeps its fixed order, so results do not depend
+  // on the split.
+  const int npull = ((flags & F_PULL) && 2 * S.maps <= tm.size) ? S.maps : 0;
+  const int wg_ranks = tm.size - npull;
+
   // ---- weight gradients
   const int n_w = L.n_pairs;
-  const Span ts = cta_span(n_w + L.maps, tm);
+  const Span ts = npull ? sub_span(n_w + L.maps, 0, wg_ranks, tm) : cta_span(n_w + L.maps, tm);
   const int p1 = min(ts.e, n_w);
   for (int c0 = ts.b; c0 < p1;) {
     int c1 = p1, da, db, need;
@@ -1311,7 +1325,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   // of the backward list times pull_g lane groups give a fixed set of streams,
   // combined in stream order -- independent of the team.
   const int G = L.pull_g, NCH = L.pull_ch, NS = NCH * G;
-  const Span ms = cta_span(S.maps, tm);
+  const Span ms = npull ? sub_span(S.maps, wg_ranks, tm.size, tm) : cta_span(S.maps, tm);
   const int per_map = NS * shw * 2;                 // stream buffers (floats)
   for (int m0 = ms.b; m0 < ms.e;) {
     int m1 = min(ms.e, m0 + max(1, nwarps / NCH));
