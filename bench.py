@@ -490,6 +490,21 @@ def run_ours(args):
                   "note": "value: deformation kernel alone (images/s); train_value: "
                           "deformation + online pass over the deformed images"}
 
+    # -- latency budget of one online step (instrumented run, outside the
+    # timed region): online training at batch 1 is bound by the chain of
+    # dependent phases and their team barriers, not by FLOPs or bytes ----
+    latency = None
+    try:
+        pw, pb = training.profile_phases(net, train.limit(min(n_img, 500)), eta)
+        latency = {"phases_per_image": int(len(pw)),
+                   "work_us_per_image": float(pw.sum()) / 1e3,
+                   "barrier_us_per_image": float(pb.sum()) / 1e3,
+                   "per_phase_us": [round(float(w) / 1e3, 2) for w in pw],
+                   "note": "slowest CTA's work per phase + the team barrier after it "
+                           "(%globaltimer, instrumented launch); the step time is their sum"}
+    except Exception as exc:          # instrumentation is diagnostic only
+        latency = {"error": str(exc)[:200]}
+
     # -- roofline of the persistent training kernel ------------------------
     props = torch.cuda.get_device_properties(local)
     sm_max = clk.get("sm_max_mhz") or 1965.0
@@ -541,6 +556,7 @@ def run_ours(args):
             "e2e": e2e,
             "committee": committee,
             "deform": deform,
+            "latency": latency,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"persistent online-training kernel ({net.kernel_info()})",
