@@ -498,13 +498,15 @@ __device__ __forceinline__ float conv_cell_smem(float acc, const float* src, con
     float xn[KK], wn[KK];
     const int kn = k + 1 < nk ? k + 1 : k;
     const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0 + 4u * kn);
+    // source k+1's loads interleaved with source k's add chain: in-order
+    // issue fills the FADD latency with the loads instead of issuing all
+    // loads first
 #pragma unroll
     for (int t = 0; t < KK; ++t) {
       xn[t] = lds_f32(sb + 4u * ((t / KX) * sw + t % KX));
       wn[t] = lds_f32(w0 + 4u * (kn * KK + t));
+      acc = __fadd_rn(acc, __fmul_rn(wc[t], xc[t]));
     }
-#pragma unroll
-    for (int t = 0; t < KK; ++t) acc = __fadd_rn(acc, __fmul_rn(wc[t], xc[t]));
 #pragma unroll
     for (int t = 0; t < KK; ++t) {
       xc[t] = xn[t];
