@@ -71,8 +71,9 @@ def all_reduce_count(count: int, group=None) -> int:
     return int(t.item())
 
 
-def _device_predictor(net, data: Dataset):
-    """Shard predictor backed by the CUDA engine (ck_net_eval)."""
+def _device_predictor(net, data: Dataset, engine: str = "exact"):
+    """Shard predictor backed by the CUDA engine (ck_net_eval, or the
+    tensor-core path with engine="tc")."""
     from .device import device_dataset, torch_cuda
     from .training import eval_range_async
 
@@ -83,22 +84,23 @@ def _device_predictor(net, data: Dataset):
         if count == 0:
             return np.zeros(0, np.int32)
         pred = torch.empty(count, dtype=torch.int32, device=torch.device("cuda", net.device))
-        eval_range_async(net, dd, first, count, pred)
+        eval_range_async(net, dd, first, count, pred, engine=engine)
         return pred.cpu().numpy()
 
     return predict
 
 
-def sharded_evaluate(net, data: Dataset, group=None, predictor=None):
+def sharded_evaluate(net, data: Dataset, group=None, predictor=None, engine: str = "exact"):
     """training.evaluate over a test set split across the ranks of ``group``.
 
     Returns (error percent, predicted labels of ALL images) on every rank.
-    ``predictor(first, count) -> labels`` defaults to the CUDA engine.
+    ``predictor(first, count) -> labels`` defaults to the CUDA engine
+    (``engine`` = "exact" bit-exact SIMT path, "tc" tensor-core path).
     """
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     first, count = shard_range(len(data), rank, world)
-    predict = predictor or _device_predictor(net, data)
+    predict = predictor or _device_predictor(net, data, engine)
     local = np.asarray(predict(first, count), dtype=np.int32)
     wrong = int(np.count_nonzero(local != data.labels[first:first + count]))
     labels = gather_shards(local, len(data), group)

@@ -46,6 +46,9 @@ def test_sharded_evaluate_equals_evaluate(nccl_world):
     err, labels = multigpu.sharded_evaluate(net, test)
     np.testing.assert_array_equal(labels, ck.predict_batch(net, test))
     assert err == ck.evaluate(net, test)
+    err_tc, labels_tc = multigpu.sharded_evaluate(net, test, engine="tc")
+    np.testing.assert_array_equal(labels_tc, ck.predict_batch(net, test, engine="tc"))
+    assert np.mean(labels_tc == labels) >= 0.995
     flat = net.flat_parameters()
     multigpu.broadcast_parameters(net, 0)
     np.testing.assert_array_equal(net.flat_parameters(), flat)
