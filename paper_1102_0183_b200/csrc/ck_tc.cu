@@ -55,6 +55,7 @@ struct GemmLayer {
   int kx, ky, tx, ty, cx, cy;  // kernel, stride (skip + 1), centre offset (contrast)
   int N, OH, OW;               // destinations, output rows / cols
   int K, K_pad, N_pad, passes, parts;    // parts: 2 (hi + lo) when passes == 3
+  int bk;                      // K per chunk: 16, 32 or 64 (small K wastes no MMA / gather work)
   int act;                     // 1: 1.7159 tanh(0.6666 a); 0: identity
   int dst_maps, dst_off;       // output tensor map count and this layer's first map
   int px, py, PH, PW;          // fused max-pool (1x1: none); output is (PH, PW)
@@ -172,13 +173,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // fp16 hi and lo parts and the MMAs Ah*Bh + Ah*Bl + Al*Bh run back to back.
 // kdec[k]: CLAMP (contrast) s<<16 | v<<8 | u; otherwise the element offset
 // s*H*W + v*W + u of the tap relative to the row's window origin; -1 = pad.
-template <bool CLAMP, bool SPLIT>
+template <bool CLAMP, bool SPLIT, int BKT>
 __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M, int tmem_cols,
                                                           int stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NP = SPLIT ? 2 : 1;                 // operand parts
-  const int a_bytes = BM * BK * 2;                  // one part of one stage
-  const int b_bytes = G.Nt * BK * 2;                // one part of one stage (a column tile)
+  constexpr int KC = BKT / 8;                       // core matrices along K per chunk
+  constexpr int RG = KC * 128;                      // bytes per 8-row group
+  const int a_bytes = BM * BKT * 2;                 // one part of one stage
+  const int b_bytes = G.Nt * BKT * 2;               // one part of one stage (a column tile)
   uint8_t* As = smem;                               // [stage][part] a_bytes
   uint8_t* Bs = smem + stages * NP * a_bytes;       // [stage][part] b_bytes (hi then lo)
   int* kdec = reinterpret_cast<int*>(Bs + stages * NP * b_bytes);
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
   const uint32_t tmem = tmem_slot;
 
   const int HW = G.H * G.W;
-  const int chunks = G.K_pad / BK;
+  const int chunks = G.K_pad / BKT;
   int64_t g = 0;                          // global chunk counter (stage phases)
 
   // M counts pool blocks: tile t holds blocks [t*bpt, (t+1)*bpt), P rows
@@ -241,17 +244,17 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
       uint8_t* a_st = As + st * NP * a_bytes;
       uint8_t* b_st = Bs + st * NP * b_bytes;
       if (tid == 0) {
-        const __half* bsrc = G.Bw + (int64_t)ch * NP * G.N_pad * BK + (int64_t)n0 * BK;
-        expect_tx(&load_bar[st], NP * nw * BK * 2);
-        bulk_copy(b_st, bsrc, nw * BK * 2, &load_bar[st]);
-        if (SPLIT) bulk_copy(b_st + b_bytes, bsrc + (int64_t)G.N_pad * BK, nw * BK * 2, &load_bar[st]);
+        const __half* bsrc = G.Bw + (int64_t)ch * NP * G.N_pad * BKT + (int64_t)n0 * BKT;
+        expect_tx(&load_bar[st], NP * nw * BKT * 2);
+        bulk_copy(b_st, bsrc, nw * BKT * 2, &load_bar[st]);
+        if (SPLIT) bulk_copy(b_st + b_bytes, bsrc + (int64_t)G.N_pad * BKT, nw * BKT * 2, &load_bar[st]);
       }
-      const int kc0 = ch * BK;
-      // all 32 loads of this thread first (latency overlap), then convert
-      float x[4][8];
+      const int kc0 = ch * BKT;
+      // all loads of this thread first (latency overlap), then convert
+      float x[KC / 2][8];
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int kg = (tid >> 7) + 2 * it;          // 0..7: core matrix along K
+      for (int it = 0; it < KC / 2; ++it) {
+        const int kg = (tid >> 7) + 2 * it;          // core matrix along K
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int dec = kdec[kc0 + kg * 8 + e];
@@ -269,9 +272,9 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
         }
       }
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
+      for (int it = 0; it < KC / 2; ++it) {
         const int kg = (tid >> 7) + 2 * it;
-        const int off = (row >> 3) * 1024 + kg * 128 + (row & 7) * 16;
+        const int off = (row >> 3) * RG + kg * 128 + (row & 7) * 16;
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
@@ -293,15 +296,15 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t ah = smem_u32(a_st), bh = smem_u32(b_st);
 #pragma unroll
-        for (int ks = 0; ks < BK / 16; ++ks) {
+        for (int ks = 0; ks < BKT / 16; ++ks) {
           const uint32_t id = instr_desc(nw);
           const uint32_t boff = ks * 256;
-          const uint64_t a_hi = umma_desc(ah + ks * 256, 128, 1024);
-          const uint64_t b_hi = umma_desc(bh + boff, 128, 1024);
+          const uint64_t a_hi = umma_desc(ah + ks * 256, 128, RG);
+          const uint64_t b_hi = umma_desc(bh + boff, 128, RG);
           mma_f16(tmem, a_hi, b_hi, id, (ch > 0 || ks > 0) ? 1 : 0);
           if (SPLIT) {
-            mma_f16(tmem, a_hi, umma_desc(bh + b_bytes + boff, 128, 1024), id, 1);
-            mma_f16(tmem, umma_desc(ah + a_bytes + ks * 256, 128, 1024), b_hi, id, 1);
+            mma_f16(tmem, a_hi, umma_desc(bh + b_bytes + boff, 128, RG), id, 1);
+            mma_f16(tmem, umma_desc(ah + a_bytes + ks * 256, 128, RG), b_hi, id, 1);
           }
         }
         mma_commit(&mma_bar[st]);
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
 // B[n, k] = src[wmap[n * K_pad + k]] (or 0) in the chunked core-matrix
 // layout: per K chunk the hi block, then (parts = 2) the lo block.
 __global__ void fill_weights(const float* __restrict__ src, const int* __restrict__ wmap, int N_pad,
-                             int K_pad, int parts, __half* __restrict__ out) {
+                             int K_pad, int parts, int bk, __half* __restrict__ out) {
   const int64_t total = (int64_t)parts * N_pad * K_pad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -385,10 +388,10 @@ __global__ void fill_weights(const float* __restrict__ src, const int* __restric
     const float w = idx >= 0 ? src[idx] : 0.f;
     const __half hi = __float2half_rn(w);
     const __half h = p == 1 ? __float2half_rn(w - __half2float(hi)) : hi;
-    const int ch = k / BK;
-    const int kk = k % BK;
-    const int64_t off = ((int64_t)ch * parts + p) * N_pad * BK +
-                        ((n >> 3) * 1024 + (kk >> 3) * 128 + (n & 7) * 16 + (kk & 7) * 2) / 2;
+    const int ch = k / bk;
+    const int kk = k % bk;
+    const int64_t off = ((int64_t)ch * parts + p) * N_pad * bk +
+                        ((n >> 3) * (bk * 16) + (kk >> 3) * 128 + (n & 7) * 16 + (kk & 7) * 2) / 2;
     out[off] = h;
   }
 }
@@ -552,7 +555,8 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
   CK_CHECK(g.P <= BM, CK_E_DIMENSION, "tensor-core eval: pool region above 128 cells");
   g.bpt = BM / g.P;
   g.K = S * kx * ky;
-  g.K_pad = (int)round_up(g.K, BK);
+  g.bk = g.K <= 16 ? 16 : g.K <= 32 ? 32 : BK;
+  g.K_pad = (int)round_up(g.K, g.bk);
   g.N_pad = (int)round_up(N, 16);
   CK_CHECK(g.N_pad <= 512, CK_E_DIMENSION, "tensor-core eval: more than 512 outputs per layer");
   CK_CHECK(kx < 256 && ky < 256 && S < 32768, CK_E_DIMENSION, "tensor-core eval: kernel too large");
@@ -568,7 +572,7 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
   st.M_per_img = (int64_t)g.PH * g.PW;   // pool blocks per image
   st.clamp = cx > 0 || cy > 0;
   auto smem_for = [&](int stages) {
-    return (size_t)stages * g.parts * ((size_t)BM * BK * 2 + (size_t)g.Nt * BK * 2) +
+    return (size_t)stages * g.parts * ((size_t)BM * g.bk * 2 + (size_t)g.Nt * g.bk * 2) +
            (size_t)((g.K_pad + 1) & ~1) * 4 + 4 * 8 + 2 * BM * 17 * 4;
   };
   // CTAs per SM: shared memory (228 KB per SM, 1 KB reserved per CTA) and
@@ -609,9 +613,14 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
 }
 
 typedef void (*GemmFn)(GemmLayer, int64_t, int, int);
-static GemmFn gemm_fn(bool clamp, bool split) {
-  if (clamp) return split ? gemm_kernel<true, true> : gemm_kernel<true, false>;
-  return split ? gemm_kernel<false, true> : gemm_kernel<false, false>;
+template <int BKT>
+static GemmFn gemm_fn_bk(bool clamp, bool split) {
+  if (clamp) return split ? gemm_kernel<true, true, BKT> : gemm_kernel<true, false, BKT>;
+  return split ? gemm_kernel<false, true, BKT> : gemm_kernel<false, false, BKT>;
+}
+static GemmFn gemm_fn(bool clamp, bool split, int bk) {
+  return bk == 16 ? gemm_fn_bk<16>(clamp, split)
+                  : bk == 32 ? gemm_fn_bk<32>(clamp, split) : gemm_fn_bk<64>(clamp, split);
 }
 
 __global__ void gather_bias(const float* __restrict__ params, const int* __restrict__ bmap, int n,
@@ -748,7 +757,7 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
   CK_CHECK(layers[n_layers - 1].kind == CK_LAYER_FC, CK_E_CONFIG, "last layer must be the output");
   for (auto& st : P->steps) {
     if (st.kind == ck::tc::ST_GEMM)
-      if (cudaSuccess != cudaFuncSetAttribute(ck::tc::gemm_fn(st.clamp, st.g.parts == 2),
+      if (cudaSuccess != cudaFuncSetAttribute(ck::tc::gemm_fn(st.clamp, st.g.parts == 2, st.g.bk),
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) return fail(ck::set_error(CK_E_CUDA, "tensor-core eval: kernel attributes"));
     if (st.kind == ck::tc::ST_CONTRAST)
       if (cudaSuccess != cudaFuncSetAttribute(ck::tc::contrast_kernel,
@@ -785,7 +794,7 @@ int ck_tc_set_params(ck_tc_eval* P, const float* params, ck_stream_t stream) {
   for (auto& st : P->steps) {
     if (st.kind != ck::tc::ST_GEMM || st.param_off < 0) continue;
     ck::tc::fill_weights<<<P->sms * 4, 256, 0, s>>>(params, st.d_wmap, st.g.N_pad, st.g.K_pad,
-                                                     st.g.parts, st.d_B);
+                                                     st.g.parts, st.g.bk, st.d_B);
     ck::tc::gather_bias<<<(st.g.N + 255) / 256, 256, 0, s>>>(params, st.d_bmap, st.g.N,
                                                              st.d_bias);
     ck::count_launch(2);
@@ -823,7 +832,7 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
         const int64_t M = nb * st.M_per_img;
         const int64_t tiles = (M + g.bpt - 1) / g.bpt * g.n_tiles;
         const int grid = (int)std::min<int64_t>(tiles, (int64_t)P->sms * st.ctas_per_sm);
-        ck::tc::gemm_fn(st.clamp, st.g.parts == 2)<<<grid, ck::tc::THREADS, st.smem, s>>>(
+        ck::tc::gemm_fn(st.clamp, st.g.parts == 2, st.g.bk)<<<grid, ck::tc::THREADS, st.smem, s>>>(
             g, M, st.tmem_cols, st.stages);
       }
       ck::count_launch();
