@@ -475,26 +475,38 @@ __global__ void __launch_bounds__(256) contrast_kernel(const float* __restrict__
   for (int i = threadIdx.x; i < F * fh * fw; i += blockDim.x) cf[i] = coef[i];
   __syncthreads();
   const int strips = (W + 3) / 4;
-  for (int job = threadIdx.x; job < F * H * strips; job += blockDim.x) {
-    const int f = job / (H * strips);
+  // filters in pairs: each window load feeds 2 filters x 4 cells
+  const int fpairs = (F + 1) / 2;
+  for (int job = threadIdx.x; job < fpairs * H * strips; job += blockDim.x) {
+    const int f0 = 2 * (job / (H * strips));
+    const bool two = f0 + 1 < F;
     const int r = (job / strips) % H;
     const int c0 = (job % strips) * 4;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc0[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};
     for (int v = 0; v < fh; ++v) {
       const float* w = win + (r + v) * PW + c0;
-      const float* k = cf + (f * fh + v) * fw;
+      const float* k0 = cf + (f0 * fh + v) * fw;
+      const float* k1 = two ? k0 + fh * fw : k0;
       float x0 = w[0], x1 = w[1], x2 = w[2], x3 = w[3];
       for (int u = 0; u < fw; ++u) {
-        const float kk = k[u];
-        acc[0] = fmaf(kk, x0, acc[0]);
-        acc[1] = fmaf(kk, x1, acc[1]);
-        acc[2] = fmaf(kk, x2, acc[2]);
-        acc[3] = fmaf(kk, x3, acc[3]);
+        const float a = k0[u], b = k1[u];
+        acc0[0] = fmaf(a, x0, acc0[0]);
+        acc0[1] = fmaf(a, x1, acc0[1]);
+        acc0[2] = fmaf(a, x2, acc0[2]);
+        acc0[3] = fmaf(a, x3, acc0[3]);
+        acc1[0] = fmaf(b, x0, acc1[0]);
+        acc1[1] = fmaf(b, x1, acc1[1]);
+        acc1[2] = fmaf(b, x2, acc1[2]);
+        acc1[3] = fmaf(b, x3, acc1[3]);
         x0 = x1; x1 = x2; x2 = x3; x3 = w[u + 4];
       }
     }
-    float* out = Y + ((img * out_maps + C + f * C + c) * (int64_t)H + r) * W;
-    for (int q = 0; q < 4 && c0 + q < W; ++q) out[c0 + q] = acc[q];
+    float* out0 = Y + ((img * out_maps + C + f0 * C + c) * (int64_t)H + r) * W;
+    float* out1 = out0 + (int64_t)C * H * W;
+    for (int q = 0; q < 4 && c0 + q < W; ++q) {
+      out0[c0 + q] = acc0[q];
+      if (two) out1[c0 + q] = acc1[q];
+    }
   }
 }
 
