@@ -20,18 +20,21 @@
 // GEMM.  Neither is bit-exact with the reference's sequential f32 chain, so
 // labels are compared by agreement rate (tests/test_gpu_tc.py).
 //
-// Per CTA (256 threads, persistent over M tiles):
+// Per CTA (256 threads, persistent over (row tile, column tile) pairs; two or
+// more CTAs per SM so one CTA's epilogue overlaps another's gather / MMAs):
 //   * all threads gather the A chunk (128 x 64 fp16) straight into shared
 //     memory in the UMMA no-swizzle K-major core-matrix layout (8 rows x 16 B
 //     per core matrix; K-adjacent cores 128 B apart, 8-row groups 1 KB apart);
 //   * thread 0 streams the matching B chunk (pre-laid-out in HBM in the same
 //     layout) with one cp.async.bulk (TMA bulk copy) onto an mbarrier;
 //   * thread 0 issues tcgen05.mma (M=128, N<=256 per instruction, K=16) for
-//     the chunk and tcgen05.commit's it onto the buffer's mbarrier, so the
-//     gather of chunk c+1 overlaps the MMAs of chunk c (double buffer);
+//     the chunk and tcgen05.commit's it onto the stage's mbarrier, so the
+//     gather of chunk c+1 overlaps the MMAs of chunk c (when two stages fit);
+//     K chunks are 16, 32 or 64 wide to match small-K first layers;
 //   * epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32*(w%4)..+31),
-//     bias + scaled tanh, store (image, map, row, col) f32.
-// Pooling and the argmax run in small SIMT kernels between the GEMMs.
+//     bias + scaled tanh, and the max-pool of the layer above fused in (M
+//     is ordered by pool blocks); store (image, map, row, col) f32.
+// Unfused pools, the contrast layer and the argmax are small SIMT kernels.
 #include <cuda_fp16.h>
 #include <math.h>
 
@@ -114,16 +117,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity));
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes));
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 
 __device__ __forceinline__ void expect_tx(uint64_t* bar, unsigned bytes) {
