@@ -32,8 +32,9 @@
 //     gather of chunk c+1 overlaps the MMAs of chunk c (when two stages fit);
 //     K chunks are 16, 32 or 64 wide to match small-K first layers;
 //   * epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32*(w%4)..+31),
-//     bias + scaled tanh, and the max-pool of the layer above fused in (M
-//     is ordered by pool blocks); store (image, map, row, col) f32.
+//     the max-pool of the layer above fused in (M is ordered by pool
+//     blocks) on the raw accumulators, then bias + scaled tanh once per
+//     pooled value (both monotone); store (image, map, row, col) f32.
 // Unfused pools, the contrast layer and the argmax are small SIMT kernels.
 #include <cuda_fp16.h>
 #include <math.h>
@@ -328,13 +329,10 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + c16 * 16, v);
         const int erow = quarter * 32 + lane;
+        // raw accumulators: bias and activation are monotone, so they are
+        // applied once per pooled value below (max(f(a_i + b)) = f(max a_i + b))
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int n = min(n0 + c16 * 16 + i, G.N - 1);
-          float a = v[i] + (G.bias ? __ldg(G.bias + n) : 0.f);
-          if (G.act) a = act_fast(a);
-          stage[erow * 17 + i] = a;
-        }
+        for (int i = 0; i < 16; ++i) stage[erow * 17 + i] = v[i];
         group_sync(grp);
         // thread -> (block b, columns i0, i0 + istep, ...): no divisions
         const int istep = BM / G.bpt;
@@ -351,7 +349,9 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_kernel(GemmLayer G, int64_t M
                 const float xv = col[w * 17];
                 if (xv > best) best = xv;
               }
-              G.Y[ob + (int64_t)n * pcells] = best;
+              float a = best + (G.bias ? __ldg(G.bias + n) : 0.f);
+              if (G.act) a = act_fast(a);
+              G.Y[ob + (int64_t)n * pcells] = a;
             }
           }
         }
