@@ -91,7 +91,10 @@ enum OpKind {
   OP_CONV_POOL,       // conv a, y fused with the max-pool above it (y, argmax)
 };
 
-enum OpFlags { F_UPDATE = 1, F_PULL = 2, F_ZERO_SELF = 4, F_FUSE_BELOW = 8 };
+// F_POOLED_ONLY (evaluation): a conv+pool keeps only the pooled values; the
+// pool picks the largest pre-activation and activates it once (the
+// activation is monotone, so the pooled value is the same bit for bit).
+enum OpFlags { F_UPDATE = 1, F_PULL = 2, F_ZERO_SELF = 4, F_FUSE_BELOW = 8, F_POOLED_ONLY = 16 };
 
 struct Op {
   int16_t kind;
@@ -710,6 +713,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
   }
   const bool whole = src != src_g;
   const bool zero = full && (flags & F_ZERO_SELF);
+  const bool pooled_only = (flags & F_POOLED_ONLY) && !full;
   // The arena is tiled like ConnectionTable (checked at ck_net_create): dest
   // map d's blocks start at fwd_off[d]*kk + d and its bias sits at
   // fwd_off[d+1]*kk + d, so the chunk plan needs fwd_off alone.
@@ -782,13 +786,19 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
             conv_block_smem<KX, KY, 4>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
           int bt = 0;
           float best = 0.0f;
-          for (int t = 0; t < blk; ++t) {   // scan order: rows, then columns
-            const int cell = d * hw + (r0 + t / P.px) * L.w + c0 + t % P.px;
-            const float yv = conv_act(acc[t]);
-            a[cell] = acc[t];
-            y[cell] = yv;
-            if (zero) dl[cell] = 0.0f;
-            if (t == 0 || yv > best) { best = yv; bt = t; }
+          if (pooled_only) {
+            for (int t = 1; t < blk; ++t)
+              if (acc[t] > acc[bt]) bt = t;
+            best = conv_act(acc[bt]);
+          } else {
+            for (int t = 0; t < blk; ++t) {   // scan order: rows, then columns
+              const int cell = d * hw + (r0 + t / P.px) * L.w + c0 + t % P.px;
+              const float yv = conv_act(acc[t]);
+              a[cell] = acc[t];
+              y[cell] = yv;
+              if (zero) dl[cell] = 0.0f;
+              if (t == 0 || yv > best) { best = yv; bt = t; }
+            }
           }
           const int r = r0 + bt / P.px, c = c0 + bt % P.px;
           pyv[qq] = best;
@@ -823,6 +833,10 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
       } else {
         acc = conv_value_global<KX, KY>(R, L, S, arena, src, d, r, c);
       }
+      if (pooled_only) {
+        ybuf[it] = acc;             // pre-activation; activated after the pool
+        continue;
+      }
       const int cell = d * hw + r * L.w + c;
       const float yv = conv_act(acc);
       a[cell] = acc;
@@ -839,6 +853,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
       float best = yb[0];
       for (int t = 1; t < blk; ++t)
         if (yb[t] > best) { best = yb[t]; bt = t; }
+      if (pooled_only) best = conv_act(best);
       const int qq = q + qi;
       const int d = qq / phw, pp = qq % phw;
       const int r = (pp / P.w) * P.py + bt / P.px;

@@ -98,7 +98,7 @@ struct ProgramBuilder {
 
 // `skip_out`: the output layer's forward is folded into OP_FC_OUT.
 void build_forward(ProgramBuilder& b, const NetGeo& N, bool load, bool zero,
-                   bool skip_out = false) {
+                   bool skip_out = false, bool pooled_only = false) {
   const int last = skip_out ? N.n_layers - 1 : N.n_layers;
   // The first layer can read the image itself (stage_input) when it is a
   // conv+pool or the contrast layer and the image fits in shared memory; the
@@ -117,7 +117,7 @@ void build_forward(ProgramBuilder& b, const NetGeo& N, bool load, bool zero,
                                 N.L[k + 1].kind == L_POOL && L.has_delta;
     if (L.kind == L_CONV && k + 1 < last && N.L[k + 1].kind == L_POOL) {
       // conv + the max-pool above it in one phase
-      b.add(OP_CONV_POOL, k, scatter_target ? F_ZERO_SELF : 0);
+      b.add(OP_CONV_POOL, k, (scatter_target ? F_ZERO_SELF : 0) | (pooled_only ? F_POOLED_ONLY : 0));
       const bool pool_target = zero && k + 2 < N.n_layers && N.L[k + 2].kind == L_POOL;
       if (pool_target) b.add(OP_ZERO_DELTA, k + 1);
       b.phase();
@@ -218,7 +218,7 @@ void build_programs(NetGeo& N, bool* ok) {
   }
   {
     ProgramBuilder b(N.prog[PROG_EVAL]);
-    build_forward(b, N, true, false);
+    build_forward(b, N, true, false, false, true);
     *ok = *ok && b.ok;
   }
 }
