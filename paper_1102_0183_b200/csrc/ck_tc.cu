@@ -168,7 +168,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // kdec[k]: CLAMP (contrast) s<<16 | v<<8 | u; otherwise the element offset
 // s*H*W + v*W + u of the tap relative to the row's window origin; -1 = pad.
 template <bool CLAMP, bool SPLIT, int BKT>
-__global__ void __launch_bounds__(THREADS, BKT == 64 ? 2 : (BKT == 32 ? 3 : 4)) gemm_kernel(GemmLayer G, int64_t M, int tmem_cols,
+__global__ void __launch_bounds__(THREADS, BKT == 64 ? 3 : 4) gemm_kernel(GemmLayer G, int64_t M, int tmem_cols,
                                                           int stages) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NP = SPLIT ? 2 : 1;                 // operand parts
@@ -590,9 +590,9 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
   };
   st.stages = occ(smem_for(2)) >= std::max(1, occ(smem_for(1))) ? 2 : 1;
   st.smem = smem_for(st.stages);
-  // registers: gemm_kernel's launch bounds give 2 / 3 / 4 CTAs of 256 threads
-  // per SM for K chunks of 64 / 32 / 16
-  const int by_regs = g.bk == 64 ? 2 : g.bk == 32 ? 3 : 4;
+  // registers: gemm_kernel's launch bounds give 3 / 4 CTAs of 256 threads
+  // per SM for K chunks of 64 / 32-or-16
+  const int by_regs = g.bk == 64 ? 3 : 4;
   st.ctas_per_sm = std::max(1, std::min(occ(st.smem), by_regs));
   CK_CHECK(st.smem <= 220 * 1024, CK_E_DIMENSION, "tensor-core eval: tile exceeds shared memory");
   std::vector<int> kdec(g.K_pad, -1);
