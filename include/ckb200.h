@@ -104,6 +104,43 @@ int ck_contrast(const float* src, int n_ch, int rows, int pitch, int w, int h,
                 const double* coeffs, int n_filters, int fh, int fw,
                 float* out, int out_rows, int out_pitch, ck_stream_t stream);
 
+/* FC-side operators.  The reference computes these inline with numpy
+ * (not through convkit.kernels); they are exported so a caller can run every
+ * layer of NetworkState.forward/backward/apply_gradients on the device.
+ * Same arithmetic as the fused engine, so results equal its bits. */
+
+/* network.py:193-199: a = x @ W + b (W is (n_in, n_out) row-major; f64
+ * accumulation, rounded once, then + b in f32), y = 1.7159*tanh(0.6666*a)
+ * in the NEP-50 f32 chain of layers.py:23-25.  a_out may be NULL. */
+int ck_fc_fwd(const float* x, int n_in, const float* weights, const float* bias, int n_out,
+              float* a_out, float* y_out, ck_stream_t stream);
+
+/* network.py:214-218 + 268-273: xgrad = W @ delta from the weights BEFORE
+ * the update (f64, rounded once; NULL to skip), grad_w = outer(x, delta),
+ * grad_b = delta (each NULL to skip), and for eta > 0 the in-place SGD step
+ * W -= f32(eta*grad_w), b -= f32(eta*grad_b).  eta == 0: no update;
+ * eta < 0: CK_E_CONFIG (network.py:266-267). */
+int ck_fc_bwd_update(const float* x, int n_in, float* weights, float* bias, int n_out,
+                     const float* delta, float* xgrad, float* grad_w, float* grad_b,
+                     double eta, ck_stream_t stream);
+
+/* layers.py:28-30 applied as network.py:219/226/251-252 do:
+ * delta *= activation_deriv(a) over the logical (w, h) cells of a pitched
+ * (maps, rows, pitch) stack; an FC vector is (1, 1, n) with w = n, h = 1. */
+int ck_act_deriv_mul(const float* a, float* delta, int n_maps, int rows, int pitch, int w,
+                     int h, ck_stream_t stream);
+
+/* network.py:268-273: params -= f32(eta * grads) element-wise (conv arenas
+ * and FC weights alike).  eta <= 0: CK_E_CONFIG. */
+int ck_sgd_update(float* params, const float* grads, int64_t n, double eta,
+                  ck_stream_t stream);
+
+/* backprop.py:22-39: delta_j = f32((y_j - t_j) * f'(a_j)) in f64 and
+ * *loss = 0.5 * sum (y - t)^2 (numpy pairwise order).  targets are f64
+ * (training.targets_for); scratch holds n doubles; loss may be NULL. */
+int ck_output_deltas(const float* y, const float* a, const double* targets, int n,
+                     float* delta, double* loss, double* scratch, ck_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * 2. Network seam (NetworkState, network.py:81-304; training.py:126-199).
  * ---------------------------------------------------------------------- */

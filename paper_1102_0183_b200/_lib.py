@@ -63,6 +63,11 @@ _SIGNATURES = {
                               _i32, _i32, _vp]),
     "ck_contrast": (_i32, [_pf, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _i32,
                            _pf, _i32, _i32, _vp]),
+    "ck_fc_fwd": (_i32, [_pf, _i32, _pf, _pf, _i32, _pf, _pf, _vp]),
+    "ck_fc_bwd_update": (_i32, [_pf, _i32, _pf, _pf, _i32, _pf, _pf, _pf, _pf, _f64, _vp]),
+    "ck_act_deriv_mul": (_i32, [_pf, _pf, _i32, _i32, _i32, _i32, _i32, _vp]),
+    "ck_sgd_update": (_i32, [_pf, _pf, _i64, _f64, _vp]),
+    "ck_output_deltas": (_i32, [_pf, _pf, _vp, _i32, _pf, _vp, _vp, _vp]),
     "ck_net_create": (_i32, [C.POINTER(LayerDesc), _i32, _i32, C.POINTER(_vp)]),
     "ck_net_destroy": (_i32, [_vp]),
     "ck_net_set_team": (_i32, [_vp, _i32, _i32, _i32]),

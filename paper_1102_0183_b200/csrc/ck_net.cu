@@ -952,7 +952,7 @@ int ck_committee_train_epoch(ck_net* const* nets, int n_nets, const uint8_t* ima
                              const float* lut, const int32_t* labels, const int32_t* order,
                              int64_t n, double eta, double* mean_losses, ck_stream_t stream) {
   CK_CHECK(nets && n_nets >= 1 && n_nets <= kMaxNetsPerLaunch, CK_E_CONFIG,
-           "need 1..64 nets");
+           "need 1..32 nets per launch (kMaxNetsPerLaunch; callers split larger committees)");
   CK_CHECK(images && labels, CK_E_CONFIG, "null dataset pointer");
   CK_CHECK(n >= 1, CK_E_CONFIG, "empty epoch");
   CK_CHECK(eta > 0, CK_E_CONFIG, "learning rate must be > 0");

@@ -215,6 +215,114 @@ __global__ void seam_contrast(const float* __restrict__ src, int n_ch,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// FC-side seam (the reference does these inline in numpy, network.py:193-199,
+// 209-230, 264-273; backprop.py:22-39).  Same arithmetic as the fused engine
+// (ck_engine.cuh fc_cols_preact / fc_bwd_rows / op_out_delta), so a layer run
+// through the seam gives the engine's bits.
+constexpr int kSeamFcSlices = 16;
+
+// a_j = f32(sum over 16 interleaved row slices of f64 fma chains) + b_j;
+// y_j = fc_act(a_j).  One thread per column (coalesced rows of W).
+__global__ void seam_fc_fwd(const float* __restrict__ x, int n_in,
+                            const float* __restrict__ W, const float* __restrict__ b,
+                            int n_out, float* a, float* y) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_out) return;
+  double part[kSeamFcSlices];
+#pragma unroll
+  for (int s = 0; s < kSeamFcSlices; ++s) part[s] = 0.0;
+  int i = 0;
+  for (; i + kSeamFcSlices <= n_in; i += kSeamFcSlices) {
+#pragma unroll
+    for (int s = 0; s < kSeamFcSlices; ++s)
+      part[s] = fma((double)x[i + s], (double)W[(int64_t)(i + s) * n_out + j], part[s]);
+  }
+#pragma unroll
+  for (int s = 0; s < kSeamFcSlices; ++s)
+    if (i + s < n_in) part[s] = fma((double)x[i + s], (double)W[(int64_t)(i + s) * n_out + j], part[s]);
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < kSeamFcSlices; ++s) acc += part[s];
+  const float aj = __fadd_rn((float)acc, b[j]);
+  if (a) a[j] = aj;
+  y[j] = fc_act(aj);
+}
+
+__device__ __forceinline__ double seam_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per input row i: xgrad_i = f32(sum_j W[i,j] delta_j) (f64, lane
+// stride + xor tree) from the OLD weights, then grad_w[i,j] = f32(x_i delta_j)
+// stored and/or applied (w -= f32(eta * g)).  Row 0's warp also does the bias.
+__global__ void seam_fc_bwd(const float* __restrict__ x, int n_in, float* W, float* b,
+                            int n_out, const float* __restrict__ delta, float* xgrad,
+                            float* grad_w, float* grad_b, float eta_f, int update) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= n_in) return;
+  float* row = W + (int64_t)i * n_out;
+  double acc = 0.0;
+  for (int j = lane; j < n_out; j += 32) acc = fma((double)row[j], (double)delta[j], acc);
+  acc = seam_warp_sum(acc);
+  if (xgrad && lane == 0) xgrad[i] = (float)acc;
+  __syncwarp();
+  const float xi = x[i];
+  for (int j = lane; j < n_out; j += 32) {
+    const float g = __fmul_rn(xi, delta[j]);
+    if (grad_w) grad_w[(int64_t)i * n_out + j] = g;
+    if (update) row[j] = sgd(row[j], eta_f, g);
+  }
+  if (i == 0) {
+    for (int j = lane; j < n_out; j += 32) {
+      if (grad_b) grad_b[j] = delta[j];
+      if (update) b[j] = sgd(b[j], eta_f, delta[j]);
+    }
+  }
+}
+
+// delta[m, r, c] = f32(delta * activation_deriv(a)) over the logical cells
+// of a pitched stack (network.py:219, 226, 251-252).
+__global__ void seam_act_deriv_mul(const float* __restrict__ a, float* delta, int n_maps,
+                                   int64_t map_stride, int pitch, int w, int h) {
+  const int64_t cells = (int64_t)n_maps * h * w;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < cells;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(q % w);
+    const int r = (int)((q / w) % h);
+    const int m = (int)(q / ((int64_t)w * h));
+    const int64_t o = m * map_stride + (int64_t)r * pitch + c;
+    delta[o] = __fmul_rn(delta[o], act_deriv(a[o]));
+  }
+}
+
+// params -= f32(eta * grads) (network.py:268-273, NEP-50 weak eta).
+__global__ void seam_sgd_update(float* params, const float* __restrict__ grads, int64_t n,
+                                float eta_f) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x)
+    params[q] = sgd(params[q], eta_f, grads[q]);
+}
+
+// output_deltas (backprop.py:22-32) in f64, rounded once; sample_loss
+// (backprop.py:35-39) = 0.5 * numpy pairwise sum of (y - t)^2.  One warp.
+__global__ void seam_output_deltas(const float* __restrict__ y, const float* __restrict__ a,
+                                   const double* __restrict__ targets, int n, float* delta,
+                                   double* loss, double* scratch) {
+  const int lane = threadIdx.x;
+  for (int j = lane; j < n; j += 32) {
+    const double r = (double)y[j] - targets[j];
+    delta[j] = (float)(r * (double)act_deriv(a[j]));
+    scratch[j] = r * r;
+  }
+  __syncwarp();
+  if (lane == 0 && loss) *loss = 0.5 * np_pairwise_sum(scratch, n);
+}
+
 static int finish_launch(const char* what) {
   count_launch();
   cudaError_t e = cudaGetLastError();
@@ -339,6 +447,55 @@ int ck_contrast(const float* src, int n_ch, int rows, int pitch, int w, int h,
       src, n_ch, (int64_t)rows * pitch, pitch, w, h, coeffs, n_filters, fh, fw, out,
       (int64_t)out_rows * out_pitch, out_pitch);
   return finish_launch("ck_contrast");
+}
+
+int ck_fc_fwd(const float* x, int n_in, const float* weights, const float* bias, int n_out,
+              float* a_out, float* y_out, ck_stream_t stream) {
+  CK_CHECK(n_in >= 1 && n_out >= 1, CK_E_DIMENSION, "FC sizes must be >= 1");
+  CK_CHECK(x && weights && bias && y_out, CK_E_CONFIG, "null FC buffer");
+  seam_fc_fwd<<<blocks_for(n_out, 128), 128, 0, (cudaStream_t)stream>>>(
+      x, n_in, weights, bias, n_out, a_out, y_out);
+  return finish_launch("ck_fc_fwd");
+}
+
+int ck_fc_bwd_update(const float* x, int n_in, float* weights, float* bias, int n_out,
+                     const float* delta, float* xgrad, float* grad_w, float* grad_b,
+                     double eta, ck_stream_t stream) {
+  CK_CHECK(n_in >= 1 && n_out >= 1, CK_E_DIMENSION, "FC sizes must be >= 1");
+  CK_CHECK(x && weights && bias && delta, CK_E_CONFIG, "null FC buffer");
+  CK_CHECK(eta >= 0.0, CK_E_CONFIG, "learning rate must be >= 0 (0 = no update)");
+  const int warps = 8;
+  seam_fc_bwd<<<blocks_for(n_in, warps), warps * 32, 0, (cudaStream_t)stream>>>(
+      x, n_in, weights, bias, n_out, delta, xgrad, grad_w, grad_b, (float)eta, eta > 0.0);
+  return finish_launch("ck_fc_bwd_update");
+}
+
+int ck_act_deriv_mul(const float* a, float* delta, int n_maps, int rows, int pitch, int w,
+                     int h, ck_stream_t stream) {
+  CK_CHECK(n_maps >= 1 && w >= 1 && h >= 1 && w <= pitch && h <= rows, CK_E_DIMENSION,
+           "bad stack geometry");
+  const int64_t cells = (int64_t)n_maps * h * w;
+  seam_act_deriv_mul<<<blocks_for(cells, 256), 256, 0, (cudaStream_t)stream>>>(
+      a, delta, n_maps, (int64_t)rows * pitch, pitch, w, h);
+  return finish_launch("ck_act_deriv_mul");
+}
+
+int ck_sgd_update(float* params, const float* grads, int64_t n, double eta,
+                  ck_stream_t stream) {
+  CK_CHECK(eta > 0.0, CK_E_CONFIG, "learning rate must be > 0");
+  if (n <= 0) return CK_OK;
+  seam_sgd_update<<<blocks_for(n, 256) < 4096 ? blocks_for(n, 256) : 4096, 256, 0,
+                    (cudaStream_t)stream>>>(params, grads, n, (float)eta);
+  return finish_launch("ck_sgd_update");
+}
+
+int ck_output_deltas(const float* y, const float* a, const double* targets, int n,
+                     float* delta, double* loss, double* scratch, ck_stream_t stream) {
+  CK_CHECK(n >= 1, CK_E_DIMENSION, "need at least one output");
+  CK_CHECK(y && a && targets && delta && scratch, CK_E_CONFIG, "null buffer");
+  seam_output_deltas<<<1, 32, 0, (cudaStream_t)stream>>>(y, a, targets, n, delta, loss,
+                                                        scratch);
+  return finish_launch("ck_output_deltas");
 }
 
 }  // extern "C"

@@ -1,42 +1,73 @@
 """Error taxonomy of the B200 engine.
 
-Mirrors the reference's exception classes (convkit ``errors.py:8-37``) so a
-caller that catches ``convkit.errors.ConfigError`` semantics gets the same
-type here, and maps the C-ABI status codes of ``include/ckb200.h`` onto them.
+Mirrors the reference's exception classes (convkit ``errors.py:8-37``) and
+maps the C-ABI status codes of ``include/ckb200.h`` onto them.
+
+When the reference package ``convkit`` is importable (the drop-in case: the
+reference's own code calls into this engine), every class here also derives
+from its ``convkit.errors`` namesake, so ``except convkit.errors.ConfigError``
+catches what this engine raises.  ``CK_STANDALONE_ERRORS=1`` opts out (and
+avoids importing convkit, which pulls in numba).
 """
 
 from __future__ import annotations
 
+import importlib.util
+import os
 
-class ConvkitError(Exception):
+
+def _reference_errors():
+    if os.environ.get("CK_STANDALONE_ERRORS") == "1":
+        return None
+    try:
+        if importlib.util.find_spec("convkit") is None:
+            return None
+        import convkit.errors as ref
+    except Exception:        # a broken or partial install: stay standalone
+        return None
+    return ref
+
+
+_REF = _reference_errors()
+
+
+def _bases(name, own):
+    """(own,) plus the reference class of the same name when available."""
+    ref = getattr(_REF, name, None) if _REF is not None else None
+    if ref is None or issubclass(own, ref):
+        return (own,)
+    return (ref,) if issubclass(ref, own) else (own, ref)
+
+
+class ConvkitError(*_bases("ConvkitError", Exception)):
     """Root of every error raised by this package."""
 
 
-class DimensionError(ConvkitError):
+class DimensionError(*_bases("DimensionError", ConvkitError)):
     """Shapes or map counts disagree."""
 
 
-class GeometryError(ConvkitError):
+class GeometryError(*_bases("GeometryError", ConvkitError)):
     """Impossible layer geometry (kernel bigger than map, size < 1, ...)."""
 
 
-class ConfigError(ConvkitError):
+class ConfigError(*_bases("ConfigError", ConvkitError)):
     """Bad configuration value or malformed architecture text."""
 
 
-class DataFormatError(ConvkitError):
+class DataFormatError(*_bases("DataFormatError", ConvkitError)):
     """Malformed dataset content."""
 
 
-class StateError(ConvkitError):
+class StateError(*_bases("StateError", ConvkitError)):
     """Call made against missing or stale runtime state."""
 
 
-class PrecisionError(ConvkitError):
+class PrecisionError(*_bases("PrecisionError", ConvkitError)):
     """The B200 path computes in FP32 only; double nets stay on the CPU."""
 
 
-class GeometryWarning(UserWarning):
+class GeometryWarning(*_bases("GeometryWarning", UserWarning)):
     """Legal but lossy geometry (fractional placement, pool truncation)."""
 
 

@@ -185,3 +185,109 @@ def contrast(src, coeffs):
               nf, fh, fw, out.data_ptr(), rows, pitch, s.stream())
     s.torch.cuda.current_stream(s.dev).synchronize()
     return out.cpu().numpy()
+
+
+# -- FC-side operators (inline numpy in the reference) --------------------------
+# network.py:193-199 (forward), :209-230 (backward), :264-273 (update) and
+# backprop.py:22-39 (output deltas, loss).  With these and the six kernels
+# above every arithmetic step of NetworkState.train_step has a device entry.
+FC_SEAM = ("fc_forward", "fc_backward", "act_deriv_mul", "sgd_update", "output_deltas")
+
+
+def _vec(t):
+    if t.dim() != 1:
+        raise DimensionError(f"expected a vector, got shape {tuple(t.shape)}")
+    return int(t.shape[0])
+
+
+def fc_forward(x, weights, bias, a_out, y_out):
+    """a = x @ W + b, y = activation(a) (network.py:197-199); W is (n_in, n_out)."""
+    s = _Staged()
+    f32 = np.float32
+    x_t, w_t, b_t = s(x, f32), s(weights, f32), s(bias, f32)
+    a_t = s(a_out, f32, out=True) if a_out is not None else None
+    y_t = s(y_out, f32, out=True)
+    n_in, n_out = _vec(x_t), _vec(b_t)
+    if tuple(w_t.shape) != (n_in, n_out) or _vec(y_t) != n_out:
+        raise DimensionError(f"FC shapes disagree: x {n_in}, W {tuple(w_t.shape)}, b {n_out}")
+    _lib.call("ck_fc_fwd", x_t.data_ptr(), n_in, w_t.data_ptr(), b_t.data_ptr(), n_out,
+              a_t.data_ptr() if a_t is not None else None, y_t.data_ptr(), s.stream())
+    s.finish()
+
+
+def fc_backward(x, weights, bias, delta, xgrad=None, grad_w=None, grad_b=None, eta=0.0):
+    """xgrad = W @ delta (old W), grad_w = outer(x, delta), grad_b = delta
+    (network.py:214-218); eta > 0 also applies the SGD step to W and b in
+    place (network.py:271-273).  Outputs left as None are skipped."""
+    if eta < 0:
+        raise ConfigError(f"learning rate must be >= 0, got {eta}")
+    s = _Staged()
+    f32 = np.float32
+    x_t, d_t = s(x, f32), s(delta, f32)
+    upd = eta > 0
+    w_t = s(weights, f32, out=upd)
+    b_t = s(bias, f32, out=upd)
+    xg = s(xgrad, f32, out=True) if xgrad is not None else None
+    gw = s(grad_w, f32, out=True) if grad_w is not None else None
+    gb = s(grad_b, f32, out=True) if grad_b is not None else None
+    n_in, n_out = _vec(x_t), _vec(d_t)
+    if tuple(w_t.shape) != (n_in, n_out) or _vec(b_t) != n_out:
+        raise DimensionError(f"FC shapes disagree: x {n_in}, W {tuple(w_t.shape)}, "
+                             f"delta {n_out}")
+    ptr = (lambda t: t.data_ptr() if t is not None else None)
+    _lib.call("ck_fc_bwd_update", x_t.data_ptr(), n_in, w_t.data_ptr(), b_t.data_ptr(), n_out,
+              d_t.data_ptr(), ptr(xg), ptr(gw), ptr(gb), float(eta), s.stream())
+    s.finish()
+
+
+def act_deriv_mul(a, delta, width=None, height=None):
+    """delta *= activation_deriv(a) (layers.py:28-30 as network.py:219/226/252
+    apply it): a vector, or a (maps, rows, pitch) stack over its logical
+    (width, height) cells (default: the whole stack)."""
+    s = _Staged()
+    a_t = s(a, np.float32)
+    d_t = s(delta, np.float32, out=True)
+    if tuple(a_t.shape) != tuple(d_t.shape):
+        raise DimensionError(f"a {tuple(a_t.shape)} and delta {tuple(d_t.shape)} differ")
+    if d_t.dim() == 1:
+        maps, rows, pitch = 1, 1, int(d_t.shape[0])
+    else:
+        maps, rows, pitch = _shape3(d_t)
+    w = pitch if width is None else int(width)
+    h = rows if height is None else int(height)
+    _lib.call("ck_act_deriv_mul", a_t.data_ptr(), d_t.data_ptr(), maps, rows, pitch, w, h,
+              s.stream())
+    s.finish()
+
+
+def sgd_update(params, grads, eta):
+    """params -= eta * grads in float32 (network.py:268-273)."""
+    if eta <= 0:
+        raise ConfigError(f"learning rate must be > 0, got {eta}")
+    s = _Staged()
+    p_t = s(params, np.float32, out=True)
+    g_t = s(grads, np.float32)
+    if p_t.numel() != g_t.numel():
+        raise DimensionError(f"{p_t.numel()} parameters vs {g_t.numel()} gradients")
+    _lib.call("ck_sgd_update", p_t.data_ptr(), g_t.data_ptr(), int(p_t.numel()), float(eta),
+              s.stream())
+    s.finish()
+
+
+def output_deltas(y, targets, a, delta_out):
+    """delta = (y - t) * f'(a) in float64 rounded to float32 (backprop.py:22-32);
+    returns sample_loss(y, t) (backprop.py:35-39)."""
+    s = _Staged()
+    y_t, a_t = s(y, np.float32), s(a, np.float32)
+    t_t = s(targets, np.float64)
+    d_t = s(delta_out, np.float32, out=True)
+    n = _vec(y_t)
+    if _vec(t_t) != n or _vec(a_t) != n or _vec(d_t) != n:
+        raise DimensionError("outputs, targets and deltas must have the same length")
+    torch = s.torch
+    loss = torch.zeros(1, dtype=torch.float64, device=s.dev)
+    scratch = torch.empty(n, dtype=torch.float64, device=s.dev)
+    _lib.call("ck_output_deltas", y_t.data_ptr(), a_t.data_ptr(), t_t.data_ptr(), n,
+              d_t.data_ptr(), loss.data_ptr(), scratch.data_ptr(), s.stream())
+    s.finish()
+    return float(loss.item())

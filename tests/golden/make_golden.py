@@ -13,6 +13,8 @@ Writes, next to this script:
                 plus dense FC buffers
   c2_traj.npz   deep-MNIST C2: 1000 online steps, weight subsamples after
                 steps 1/10/100/1000, per-step losses (BASELINE configs[1])
+  traj_<C>.npz  C3 / C4 / C4': multi-step online trajectories (weights after
+                steps 1/10/half/all, losses, test labels and outputs)
   deform.npz    augment.sample_params / deform_channels on C1/C3/C4-shaped
                 glyphs under several DeformationConfigs, and one deformed
                 online epoch of a small net (training.py:140-144)
@@ -52,7 +54,14 @@ CONFIGS = {
     "C2": "input 1x29x29; conv 40M k4x4 s0x0; maxpool 2x2; conv 60M k5x5 s0x0; maxpool 3x3; fc 150N; output 10",
     "C3": "input 2x48x48; imgproc hat21; conv 50M k5x5 s0x0; maxpool 2x2; conv 50M k5x5 s0x0; maxpool 4x4; fc 300N; output 6",
     "C4": "input 3x32x32; conv 300M k3x3 s0x0; maxpool 2x2; conv 300M k2x2 s0x0 rand30; maxpool 2x2; conv 300M k3x3 s0x0 rand30; maxpool 2x2; fc 300N; output 10",
+    # C4' (SURVEY §8d stress case): the same net with full connection tables
+    # (topology.py:126-130 build_full_table)
+    "C4F": "input 3x32x32; conv 300M k3x3 s0x0; maxpool 2x2; conv 300M k2x2 s0x0; maxpool 2x2; conv 300M k3x3 s0x0; maxpool 2x2; fc 300N; output 10",
 }
+
+# multi-step online trajectories of the larger BASELINE nets (VERDICT r1:
+# C2 alone had one): (init seed, online steps, distinct train images, test images)
+TRAJ = {"C3": (7, 200, 100, 60), "C4": (7, 200, 100, 60), "C4F": (7, 100, 50, 40)}
 
 
 def digest(a) -> str:
@@ -290,6 +299,41 @@ def c2_trajectory(steps=1000, n_images=200):
 
 
 
+def trajectory(name, seed, steps, n_images, n_test):
+    """`steps` online steps of config `name` (network.py:275-282), images
+    visited cyclically without shuffling; weight subsamples + digests after
+    steps 1/10/steps/2/steps, per-step losses, test labels and outputs."""
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        spec = ck.parse_architecture(CONFIGS[name])
+    c, w = spec.layers[0].out_maps, spec.layers[0].out_width
+    n_cls = spec.n_classes
+    net = ck.NetworkState(spec, seed, dtype=F32)
+    imgs, labels = glyph_images(n_images, n_cls, w, c, seed=1)
+    x = ck.from_bytes(imgs, labels, n_cls, "train", F32).images
+    test_u8, test_lab = glyph_images(n_test, n_cls, w, c, seed=1, split="test")
+    xt = ck.from_bytes(test_u8, test_lab, n_cls, "test", F32).images
+    rng = np.random.default_rng(2025)
+    out = {"arch": np.array(CONFIGS[name]), "seed": np.array(seed), "steps": np.array(steps),
+           "images_u8": imgs, "labels": labels, "test_u8": test_u8, "test_labels": test_lab}
+    sel = rng.choice(net.count_parameters(), size=8192, replace=False)
+    out["psel"] = sel
+    checkpoints = (1, 10, steps // 2, steps)
+    out["checkpoints"] = np.array(checkpoints)
+    losses = []
+    for step in range(1, steps + 1):
+        i = (step - 1) % n_images
+        losses.append(net.train_step(x[i], ck.targets_for(int(labels[i]), n_cls), 1e-3))
+        if step in checkpoints:
+            flat = flat_params(net)
+            out[f"params_sub_{step}"] = flat[sel]
+            out[f"params_digest_{step}"] = np.array(digest(flat))
+    out["losses"] = np.array(losses)
+    out["test_pred"] = np.array([net.predict(xt[i]) for i in range(len(xt))])
+    out["test_out"] = np.stack([net.forward(xt[i]).copy() for i in range(len(xt))])
+    return out
+
+
 def deform_cases(n_images=6, seed=5, epoch=2):
     from convkit import augment
     out = {}
@@ -322,8 +366,9 @@ def deform_cases(n_images=6, seed=5, epoch=2):
     return out
 
 
-def main(which=("kernels", "nets", "configs", "c2", "deform")):
-    kernels.set_workers(1)
+def main(which=("kernels", "nets", "configs", "c2", "deform", "traj")):
+    # results are bit-identical for every worker count (kernels.py:1-10)
+    kernels.set_workers(int(os.environ.get("CK_GOLDEN_WORKERS", "1")))
     if "kernels" in which:
         np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernel_cases())
         print("kernels.npz written")
@@ -339,7 +384,12 @@ def main(which=("kernels", "nets", "configs", "c2", "deform")):
     if "deform" in which:
         np.savez_compressed(os.path.join(HERE, "deform.npz"), **deform_cases())
         print("deform.npz written")
+    if "traj" in which:
+        for name, (seed, steps, n_images, n_test) in TRAJ.items():
+            np.savez_compressed(os.path.join(HERE, f"traj_{name}.npz"),
+                                **trajectory(name, seed, steps, n_images, n_test))
+            print(f"traj_{name}.npz written")
 
 
 if __name__ == "__main__":
-    main(tuple(sys.argv[1:]) or ("kernels", "nets", "configs", "c2", "deform"))
+    main(tuple(sys.argv[1:]) or ("kernels", "nets", "configs", "c2", "deform", "traj"))

@@ -1,6 +1,8 @@
 """bench.py keeps the driver's contract: one JSON line on stdout with the
 required keys, a roofline / cpu_baseline / e2e / clocks / gpu_launches block,
-and the reference arm's line (rank 0, CPU oracle port)."""
+the per-config blocks, and the reference arm's line (rank 0: the reference
+itself from baseline/_ref when importable, else the oracle port) with the same
+config object."""
 
 from __future__ import annotations
 
@@ -30,18 +32,25 @@ def run_bench(*args):
     return json.loads(lines[0])
 
 
+FOUR = ("value", "roofline", "cpu_baseline", "e2e")
+
+
 def test_bench_line_contract():
-    d = run_bench("--config", "C1", "--steps", "2", "--warmup", "3", "--imgs-per-step", "200",
-                  "--cpu-seconds", "1", "--no-committee")
+    d = run_bench("--config", "C1", "--blocks", "C2", "--steps", "3", "--warmup", "3",
+                  "--imgs-per-step", "64", "--cpu-seconds", "0.3", "--cpu-windows", "1")
     for k in REQUIRED:
         assert k in d, k
-    assert d["value"] > 0 and d["gpu_launches"] >= 2
+    assert d["value"] > 0 and d["gpu_launches"] == 3
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert 0 < d["roofline"]["frac"] < 1
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["eval_tc"]["label_agreement_with_exact"] >= 0.995
     assert d["deform"]["value"] > 0
     assert d["latency"]["phases_per_image"] >= 2
+    for blk in (d, d["eval"], d["configs"]["C2"], d["configs"]["C2"]["eval"], d["committee"]):
+        for k in FOUR:
+            assert blk.get(k) is not None, k
+    assert 0 < d["eval"]["roofline"]["frac"] < 1
 
 
 def test_reference_arm_line():
@@ -49,3 +58,7 @@ def test_reference_arm_line():
                   "--imgs-per-step", "16")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+    ours = run_bench("--config", "C1", "--blocks", "", "--steps", "3", "--warmup", "3",
+                     "--imgs-per-step", "16", "--no-cpu-baseline", "--no-committee",
+                     "--no-deform", "--no-tc", "--no-e2e")
+    assert d["config"] == ours["config"]          # same step definition in both arms

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import paper_1102_0183_b200 as ck
+from paper_1102_0183_b200 import configs
 from paper_1102_0183_b200 import _lib
 from paper_1102_0183_b200.errors import (ConfigError, GeometryError, GeometryWarning,
                                          PrecisionError)
@@ -112,7 +113,7 @@ def test_random_table_degree_coverage_and_seed():
 
 def test_tables_match_reference_digests(golden):
     g = golden("configs")
-    for cfg in ("C1", "C2", "C3", "C4"):
+    for cfg in ("C1", "C2", "C3", "C4", "C4F"):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             spec = ck.parse_architecture(str(g[f"{cfg}_arch"]))
@@ -172,7 +173,7 @@ def test_network_rejects_double_precision():
 def test_init_matches_reference_digest(golden):
     from oracle import oracle
     g = golden("configs")
-    for cfg in ("C1", "C4"):
+    for cfg in ("C1", "C4", "C4F"):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             spec = ck.parse_architecture(str(g[f"{cfg}_arch"]))
@@ -233,3 +234,36 @@ def test_oracle_c2_trajectory_matches_reference(golden):
     xt = ck.byte_lut()[g["test_u8"]]
     pred = [net.predict(xt[i]) for i in range(len(xt))]
     np.testing.assert_array_equal(pred, g["test_pred"])
+
+
+# -- oracle trajectories of the larger nets (tests/golden/traj_<C>.npz) -------
+
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C4F"])
+def test_oracle_trajectory_matches_reference(golden, cfg):
+    """C3 / C4 (200 online steps) and C4' (100): the oracle's weights follow
+    the reference's to 1e-6 at every checkpoint, test labels identical."""
+    from oracle import oracle
+    g = golden(f"traj_{cfg}")
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        spec = ck.parse_architecture(str(g["arch"]))
+    assert str(g["arch"]) == configs.ARCH[cfg]
+    net = oracle.OracleNet(spec, int(g["seed"]))
+    x = ck.byte_lut()[g["images_u8"]]
+    labels = g["labels"]
+    n_cls = spec.n_classes
+    steps = int(g["steps"])
+    checkpoints = set(g["checkpoints"].tolist())
+    losses = []
+    for step in range(1, steps + 1):
+        i = (step - 1) % len(labels)
+        losses.append(net.train_step(x[i], oracle.targets_for(int(labels[i]), n_cls), 1e-3))
+        if step in checkpoints:
+            got = net.flat_parameters()[g["psel"]]
+            np.testing.assert_allclose(got, g[f"params_sub_{step}"], rtol=0, atol=1e-6,
+                                       err_msg=f"step {step}")
+    np.testing.assert_allclose(losses, g["losses"], rtol=1e-5)
+    xt = ck.byte_lut()[g["test_u8"]]
+    out = np.stack([net.forward(xt[i]).copy() for i in range(len(xt))])
+    np.testing.assert_allclose(out, g["test_out"], rtol=0, atol=1e-5)
+    np.testing.assert_array_equal(out.argmax(axis=1), g["test_pred"])

@@ -146,7 +146,7 @@ def test_oracle_net_online_run_matches_reference(golden, name):
     np.testing.assert_array_equal(pred, g[p + "pred31"])
 
 
-@pytest.mark.parametrize("cfg", ("C1", "C2", "C3", "C4"))
+@pytest.mark.parametrize("cfg", ("C1", "C2", "C3", "C4", "C4F"))
 def test_oracle_configs_match_reference(golden, cfg):
     g = golden("configs")
     p = f"{cfg}_"
