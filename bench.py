@@ -88,6 +88,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-committee", action="store_true")
     ap.add_argument("--no-deform", action="store_true")
     ap.add_argument("--no-tc", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo rehearsal of the multi-rank control flow (tests)")
     return ap.parse_args(argv)
 
 
@@ -432,6 +434,32 @@ class Ctx:
                               f"x {sm_mhz:.0f} MHz (MEASURED_PEAKS.json has no FP32 figure)"}
 
 
+def eval_shard(ctx, n_images):
+    """This rank's contiguous test-set shard and the gather buffers
+    (multigpu.shard_range: ceil split, the last shards may be short/empty)."""
+    from paper_1102_0183_b200.multigpu import shard_range
+    torch = ctx.torch
+    per = (n_images + ctx.world - 1) // ctx.world
+    first, mine = shard_range(n_images, ctx.rank, ctx.world)
+    pred = torch.zeros(per, dtype=torch.int32, device=ctx.dev)
+    gathered = torch.zeros(per * ctx.world, dtype=torch.int32, device=ctx.dev)
+    wrong = torch.zeros(1, dtype=torch.int64, device=ctx.dev)
+    return first, mine, pred, gathered, wrong
+
+
+def sharded_eval_step(ctx, predict_into, labels, first, mine, pred, gathered, wrong):
+    """One sharded evaluation: predict this rank's shard into `pred`, count
+    its errors, then all-gather the labels and all-reduce the error count."""
+    if mine:
+        predict_into(first, mine, pred)
+    wrong.copy_((pred[:mine] != labels[first:first + mine]).sum().reshape(1))
+    if ctx.use_dist:
+        ctx.dist.all_gather_into_tensor(gathered, pred)
+        ctx.dist.all_reduce(wrong)
+    else:
+        gathered.copy_(pred)
+
+
 def _traffic(name, n_img, kind="train"):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(tpath):
@@ -495,11 +523,7 @@ def measure_config(ctx, name, steps, warmup, sm_mhz, full):
     # -- sharded test-set evaluation + NCCL gather --------------------------
     test = make_data(spec, TEST_IMAGES, 1, "test")
     tdd = DeviceDataset(test, ctx.local)
-    per = (TEST_IMAGES + ctx.world - 1) // ctx.world
-    first = min(ctx.rank * per, TEST_IMAGES)
-    mine = max(0, min(per, TEST_IMAGES - first))
-    pred = torch.zeros(per, dtype=torch.int32, device=ctx.dev)
-    gathered = torch.zeros(per * ctx.world, dtype=torch.int32, device=ctx.dev)
+    first, mine, pred, gathered, wrong = eval_shard(ctx, TEST_IMAGES)
     if ctx.use_dist:     # evaluate one committee member everywhere: rank 0's weights
         flat = torch.from_numpy(net.flat_parameters()).to(ctx.dev)
         ctx.dist.broadcast(flat, 0)
@@ -507,18 +531,11 @@ def measure_config(ctx, name, steps, warmup, sm_mhz, full):
         eval_net.set_flat_parameters(flat.cpu().numpy())
     else:
         eval_net = net
-    wrong = torch.zeros(1, dtype=torch.int64, device=ctx.dev)
 
     def eval_step(engine):
-        if mine:
-            training.eval_range_async(eval_net, tdd, first, mine, pred, stream=ctx.sh,
-                                      engine=engine)
-        wrong.copy_((pred[:mine] != tdd.labels[first:first + mine]).sum().reshape(1))
-        if ctx.use_dist:
-            ctx.dist.all_gather_into_tensor(gathered, pred)
-            ctx.dist.all_reduce(wrong)
-        else:
-            gathered.copy_(pred)
+        sharded_eval_step(ctx, lambda f, n, out: training.eval_range_async(
+            eval_net, tdd, f, n, out, stream=ctx.sh, engine=engine),
+            tdd.labels, first, mine, pred, gathered, wrong)
 
     ev_steps = steps if full else max(3, min(steps, 5))
     ev_ms, ev_total = ctx.timed(lambda k: eval_step("exact"), ev_steps, max(3, warmup))
@@ -534,18 +551,24 @@ def measure_config(ctx, name, steps, warmup, sm_mhz, full):
                                         "reference order, no FMA)",
                                         _traffic(name, TEST_IMAGES, "eval"))}
     ev["e2e"] = None
-    if not args.no_e2e and ctx.world == 1:
+    if not args.no_e2e:
+        from paper_1102_0183_b200 import multigpu
         host_test = pin_dataset(make_data(spec, TEST_IMAGES, 1, "test"))
 
         def eval_e2e(k):
             host_test._device_cache.clear()
-            ck.evaluate(eval_net, host_test)            # labels back to the host
+            if ctx.use_dist:                           # shards + NCCL, labels to the host
+                multigpu.sharded_evaluate(eval_net, host_test)
+            else:
+                ck.evaluate(eval_net, host_test)        # labels back to the host
 
         _, ee_total = ctx.timed(eval_e2e, ev_steps, max(3, warmup))
         ev["e2e"] = {"value": TEST_IMAGES * ev_steps / (ee_total / 1e3), "unit": UNIT,
                      "h2d_bytes_per_step": upload_bytes(host_test),
                      "d2h_bytes_per_step": 4 * TEST_IMAGES,
-                     "api": "paper_1102_0183_b200.evaluate(net, host Dataset)"}
+                     "api": "paper_1102_0183_b200.multigpu.sharded_evaluate(net, host "
+                            "Dataset)" if ctx.use_dist else
+                            "paper_1102_0183_b200.evaluate(net, host Dataset)"}
     block["eval"] = ev
 
     # -- the same evaluation on the tensor cores ----------------------------
@@ -787,6 +810,86 @@ def run_ours(args):
         ctx.dist.destroy_process_group()
 
 
+class DryCtx(Ctx):
+    """Ctx on CPU over gloo with wall-clock timing: the --dry-run rehearsal
+    of the N-rank control flow (rank roles, shards, collectives, max over
+    ranks, rank-0 output) without a GPU (tests/test_multigpu_host.py)."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.args = args
+        self.rank, self.world, self.local = dist_env()
+        if self.world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={self.world}")
+        self.dev = torch.device("cpu")
+        self.use_dist = self.world > 1 or "RANK" in os.environ
+        if self.use_dist:
+            dist.init_process_group("gloo")
+        self.sms = 148
+
+    def barrier(self):
+        if self.use_dist:
+            self.dist.barrier()
+
+    def timed(self, fn, steps, warmup):
+        for w in range(warmup):
+            fn(w)
+        self.barrier()
+        ms = []
+        for k in range(steps):
+            t0 = time.perf_counter()
+            fn(k)
+            ms.append(1e3 * (time.perf_counter() - t0))
+        self.barrier()
+        return ms, self.max_over_ranks(sum(ms))
+
+
+def run_dry(args):
+    """Stand-in work, real multi-rank plumbing: each rank 'trains' its own net
+    (weak scaling, rank-dependent duration so max-over-ranks matters), the
+    test set is evaluated in shards with a stand-in predictor, gathered and
+    reduced, committee members are split with multigpu.nets_for_rank."""
+    from paper_1102_0183_b200 import multigpu
+    ctx = DryCtx(args)
+    torch = ctx.torch
+    n_img = args.imgs_per_step
+    step_ms, total = ctx.timed(lambda k: time.sleep(0.002 * (1 + ctx.rank)), args.steps,
+                               args.warmup)
+    labels = torch.as_tensor(np.arange(TEST_IMAGES) % 10, dtype=torch.int32)
+    first, mine, pred, gathered, wrong = eval_shard(ctx, TEST_IMAGES)
+
+    def predict_into(f, n, out):
+        idx = torch.arange(f, f + n, dtype=torch.int32)
+        out[:n] = torch.where(idx % 7 == 3, (idx + 1) % 10, idx % 10)
+
+    sharded_eval_step(ctx, predict_into, labels, first, mine, pred, gathered, wrong)
+    weights = torch.full((5,), float(ctx.rank))
+    if ctx.use_dist:
+        ctx.dist.broadcast(weights, 0)
+    members = multigpu.nets_for_rank(8, ctx.rank, ctx.world)
+    counts = torch.tensor([len(members)], dtype=torch.int64)
+    if ctx.use_dist:
+        ctx.dist.all_reduce(counts)
+    if ctx.rank == 0:
+        line = {"metric": METRIC, "value": ctx.world * n_img * args.steps / (total / 1e3),
+                "unit": UNIT, "n_gpus": ctx.world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": total / args.steps, "dry_run": True,
+                "my_ms_per_step": sum(step_ms) / args.steps,
+                "eval": {"labels": gathered[:TEST_IMAGES].tolist()[:50],
+                         "labels_ok": bool((gathered[:TEST_IMAGES] ==
+                                            torch.where(torch.arange(TEST_IMAGES) % 7 == 3,
+                                                        (torch.arange(TEST_IMAGES) + 1) % 10,
+                                                        torch.arange(TEST_IMAGES) % 10)
+                                            ).all()),
+                         "wrong": int(wrong.item())},
+                "broadcast_weights": weights.tolist(), "committee_members": int(counts.item())}
+        print(json.dumps(line), file=_OUT, flush=True)
+    if ctx.use_dist:
+        ctx.dist.destroy_process_group()
+
+
 def _stdout_for_json_only():
     """Route everything native code prints (NCCL's version banner, ...) to
     stderr; return a writer for the original stdout, which gets the JSON line
@@ -803,6 +906,8 @@ def main(argv=None):
     _OUT = _stdout_for_json_only()
     if args.impl == "reference":
         run_reference(args)
+    elif args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)
 

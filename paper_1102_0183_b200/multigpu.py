@@ -118,35 +118,50 @@ def broadcast_parameters(net, src: int = 0, group=None) -> None:
 
 
 def run_committee(spec, train_data: Dataset, test_data: Dataset, config, runs: int,
-                  group=None, **net_kwargs):
-    """run_experiment with the committee split over the ranks: rank r trains
-    members nets_for_rank(runs, r, world) (seeds config.seed + member) in one
-    launch per epoch, evaluates them, and the per-member test errors and
-    predicted labels are all-gathered.  Returns (test error % per member,
-    labels (runs, n_test)) on every rank -- the values a single-GPU
-    run_experiment produces."""
+                  group=None, backend=None, **net_kwargs):
+    """run_experiment (training.py:181-199) with the committee split over the
+    ranks of ``group``: rank r trains members nets_for_rank(runs, r, world)
+    (seeds config.seed + member) together, one launch per epoch, with
+    run_training's protocol per member (validation on the training set every
+    epoch, the test set on the test_every cadence, TfbV / bT).  Each rank's
+    per-epoch errors and final test labels are all-gathered, so every rank
+    returns (ExperimentSummary, final test labels (runs, n_test)) -- the same
+    values a single-process run_experiment produces for the same seeds."""
+    import torch
     import torch.distributed as dist
 
-    from .network import NetworkState
-    from .training import predict_batch, train_committee_epoch
+    from .training import CudaBackend, EpochStats, RunRecord, committee_records, summarize
 
+    if runs < 1:
+        raise ConfigError(f"need at least one run, got {runs}")
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     mine = nets_for_rank(runs, rank, world)
-    nets = [NetworkState(spec, config.seed + m, **net_kwargs) for m in mine]
-    for epoch in range(config.epochs):
-        if nets:
-            train_committee_epoch(nets, train_data, config, epoch)
-    errs = np.zeros(runs, dtype=np.int64)
-    labels = np.zeros((runs, len(test_data)), dtype=np.int32)
-    for m, net in zip(mine, nets):
-        labels[m] = predict_batch(net, test_data)
-        errs[m] = int(np.count_nonzero(labels[m] != test_data.labels))
-        net.close()
-    # members are disjoint across ranks: a sum-reduce assembles them
-    import torch
+    backend = backend or CudaBackend(**net_kwargs)
+    records, labels = committee_records(spec, train_data, test_data, config,
+                                        [config.seed + m for m in mine], backend)
+    per = (runs + world - 1) // world           # member slots per rank (padded)
+    ep = config.epochs
     dev = _backend_device(group)
-    t_err = torch.as_tensor(errs, device=dev)
-    t_lab = torch.as_tensor(labels, device=dev)
-    dist.all_reduce(t_err, group=group)
-    dist.all_reduce(t_lab, group=group)
-    return 100.0 * t_err.cpu().numpy() / len(test_data), t_lab.cpu().numpy()
+    stats = torch.zeros((per, ep, 4), dtype=torch.float64, device=dev)
+    lab = torch.zeros((per, len(test_data)), dtype=torch.int32, device=dev)
+    for j, rec in enumerate(records):
+        stats[j] = torch.as_tensor([[st.lr, st.train_err, st.test_err, st.seconds]
+                                    for st in rec.epochs], dtype=torch.float64, device=dev)
+        lab[j] = torch.as_tensor(labels[j], device=dev)
+    all_stats = torch.zeros((world * per, ep, 4), dtype=torch.float64, device=dev)
+    all_lab = torch.zeros((world * per, len(test_data)), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(all_stats, stats, group=group)
+    dist.all_gather_into_tensor(all_lab, lab, group=group)
+    all_stats = all_stats.cpu().numpy()
+    all_lab = all_lab.cpu().numpy()
+    out_records, out_labels = [], np.zeros((runs, len(test_data)), dtype=np.int32)
+    for r in range(world):
+        for j, m in enumerate(nets_for_rank(runs, r, world)):
+            rec = RunRecord()
+            for e in range(ep):
+                lr, tr, te, sec = all_stats[r * per + j, e]
+                rec.epochs.append(EpochStats(e, float(lr), float(tr), float(te), float(sec)))
+            rec.finalize()
+            out_records.append(rec)
+            out_labels[m] = all_lab[r * per + j]
+    return summarize(out_records, [config.seed + m for m in range(runs)]), out_labels

@@ -60,11 +60,17 @@ def test_committee_equals_run_experiment(nccl_world):
     train = ck.make_glyph_dataset(120, 10, 29, seed=3)
     test = ck.make_glyph_dataset(200, 10, 29, seed=3, split="test")
     cfg = ck.TrainConfig(epochs=2, eta0=1e-3, seed=5, test_every=1)
-    errs, labels = multigpu.run_committee(spec, train, test, cfg, runs=3)
+    summary, labels = multigpu.run_committee(spec, train, test, cfg, runs=3)
+    solo = ck.run_experiment(spec, train, test, cfg, runs=3)
+    assert summary.seeds == solo.seeds
+    for got, want in zip(summary.runs, solo.runs):
+        assert [(e.train_err, e.test_err) for e in got.epochs] == \
+            [(e.train_err, e.test_err) for e in want.epochs]
+        assert (got.tfbv, got.bt, got.best_epoch) == (want.tfbv, want.bt, want.best_epoch)
     for m in range(3):
         net = ck.NetworkState(spec, cfg.seed + m)
         for e in range(cfg.epochs):
             ck.train_epoch(net, train, cfg, e)
         np.testing.assert_array_equal(labels[m], ck.predict_batch(net, test))
-        assert errs[m] == ck.evaluate(net, test)
+        assert summary.runs[m].epochs[-1].test_err == ck.evaluate(net, test)
         net.close()

@@ -94,3 +94,106 @@ def test_sharded_evaluation_matches_single_process(tmp_path, n_images):
         assert float(got["err"]) == want_err
         assert np.array_equal(got["pred"], want_pred)
         assert np.array_equal(got["flat"], want_flat)
+
+
+# -- the committee driver over gloo with a stand-in backend ----------------------
+
+class _FakeBackend:
+    """Deterministic stand-in for the CUDA engine: a 'net' is its seed plus
+    the epochs it has seen; its predictions depend on both."""
+
+    def create(self, spec, seed):
+        return {"seed": seed, "epochs": 0}
+
+    def train_epoch(self, nets, data, config, epoch):
+        for n in nets:
+            assert n["epochs"] == epoch
+            n["epochs"] += 1
+
+    def predict(self, net, data):
+        idx = np.arange(len(data))
+        wrong = (idx * (net["seed"] + 3) + net["epochs"] * 5) % 11 == 0
+        return np.where(wrong, (data.labels + 1) % 10, data.labels).astype(np.int32)
+
+    def close(self, net):
+        net["closed"] = True
+
+
+def _committee_data():
+    train = ck.Dataset(np.zeros((37, 1, 2, 2), np.float32), np.arange(37) % 10, 10, "train")
+    test = ck.Dataset(np.zeros((23, 1, 2, 2), np.float32), (np.arange(23) * 3) % 10, 10, "test")
+    return train, test
+
+
+def _committee_worker(rank, world, port, runs, out_dir):
+    import torch.distributed as dist
+
+    from paper_1102_0183_b200 import multigpu
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        train, test = _committee_data()
+        cfg = ck.TrainConfig(epochs=3, eta0=1e-3, seed=4, test_every=2)
+        summary, labels = multigpu.run_committee(None, train, test, cfg, runs,
+                                                 backend=_FakeBackend())
+        errs = np.array([[(e.train_err, e.test_err) for e in r.epochs] for r in summary.runs])
+        np.savez(os.path.join(out_dir, f"c{rank}.npz"), errs=errs, labels=labels,
+                 tfbv=[r.tfbv for r in summary.runs], bt=[r.bt for r in summary.runs],
+                 best=[r.best_epoch for r in summary.runs], seeds=summary.seeds,
+                 mean=summary.tfbv_mean)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("runs", [3, 1, 4])
+def test_run_committee_matches_single_process(tmp_path, runs):
+    """training.run_experiment's protocol split over 2 ranks (gloo) gives the
+    single-process per-epoch errors, TfbV / bT and final labels on every rank."""
+    from paper_1102_0183_b200.training import committee_records, summarize
+    world = 2
+    mp.spawn(_committee_worker, args=(world, _free_port(), runs, str(tmp_path)), nprocs=world)
+    train, test = _committee_data()
+    cfg = ck.TrainConfig(epochs=3, eta0=1e-3, seed=4, test_every=2)
+    seeds = [cfg.seed + r for r in range(runs)]
+    records, labels = committee_records(None, train, test, cfg, seeds, _FakeBackend())
+    want = summarize(records, seeds)
+    errs = np.array([[(e.train_err, e.test_err) for e in r.epochs] for r in want.runs])
+    for r in range(world):
+        got = np.load(tmp_path / f"c{r}.npz")
+        np.testing.assert_array_equal(got["errs"], errs)      # NaN where untested
+        np.testing.assert_array_equal(got["labels"], labels)
+        np.testing.assert_array_equal(got["tfbv"], [x.tfbv for x in want.runs])
+        np.testing.assert_array_equal(got["bt"], [x.bt for x in want.runs])
+        np.testing.assert_array_equal(got["best"], [x.best_epoch for x in want.runs])
+        np.testing.assert_array_equal(got["seeds"], seeds)
+        assert float(got["mean"]) == want.tfbv_mean
+
+
+# -- bench.py's N>1 control flow, rehearsed on CPU over gloo ---------------------
+
+def test_bench_dry_run_two_ranks():
+    """torchrun --nproc-per-node 2 bench.py --gpus 2 --dry-run: one JSON line
+    (rank 0 only), value from the MAX over ranks, sharded labels gathered in
+    order, errors reduced, rank 0's weights broadcast, committee split."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+         os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "4", "--warmup", "3",
+         "--dry-run"], capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"]
+    # rank 1 sleeps twice as long: the reported time is its (the max), not rank 0's
+    assert d["ms_per_step"] >= 1.8 * d["my_ms_per_step"]
+    assert d["eval"]["labels_ok"]
+    idx = np.arange(10_000)
+    assert d["eval"]["wrong"] == int(np.count_nonzero(idx % 7 == 3))
+    assert d["broadcast_weights"] == [0.0] * 5
+    assert d["committee_members"] == 8
