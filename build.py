@@ -29,6 +29,9 @@ COMPILE_FLAGS = [
     "-I", os.path.join(ROOT, "include"),
 ]
 LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared"]
+# per-unit extras: the tensor-core GEMMs run at register caps set by their
+# launch bounds (3-4 CTAs per SM); a spill there must fail the build
+UNIT_FLAGS = {"ck_tc.cu": ["-Xptxas=-warn-spills,-Werror"]}
 
 
 def _nvcc() -> str:
@@ -61,7 +64,8 @@ def _compile(out: str, verbose: bool, extra=(), specs: bool = True) -> None:
         procs = []
         for u in units:
             obj = os.path.join(tmp, os.path.basename(u) + ".o")
-            cmd = [_nvcc(), *COMPILE_FLAGS, *extra, "-c", "-o", obj, u]
+            cmd = [_nvcc(), *COMPILE_FLAGS, *extra, *UNIT_FLAGS.get(os.path.basename(u), []),
+                   "-c", "-o", obj, u]
             if verbose:
                 cmd.insert(1, "-Xptxas=-v")
             procs.append((obj, subprocess.Popen(cmd)))

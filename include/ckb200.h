@@ -192,7 +192,10 @@ int ck_net_set_params(ck_net* net, const float* host, int64_t n);
 int ck_net_get_params(ck_net* net, float* host, int64_t n);
 
 /* Per-sample calls with HOST buffers (synchronous). x is (C, H, W) dense f32,
- * targets n_classes f64.  forward writes the output activations. */
+ * targets n_classes f64.  forward writes the output activations.  These (and
+ * set/get_params, read_buffer) first wait for the whole device, so they are
+ * ordered after any asynchronous work a caller enqueued on its own streams
+ * (ck_net_train_epoch / ck_net_eval / ck_committee_train_epoch). */
 int ck_net_forward(ck_net* net, const float* x, float* y_out);
 int ck_net_backward(ck_net* net, const double* targets); /* fills grads */
 int ck_net_apply_gradients(ck_net* net, double eta);     /* w -= f32(eta)*g */

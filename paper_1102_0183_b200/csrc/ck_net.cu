@@ -372,6 +372,17 @@ Job empty_job(int prog) {
   return j;
 }
 
+// The per-sample / host-buffer API runs on the net's private stream; work a
+// caller enqueued on ITS streams (ck_net_train_epoch, ck_net_eval, ... with a
+// user stream) may still be reading or writing this net.  Every synchronous
+// entry therefore waits for the whole device first (no ordering
+// existed between the two), and ends with its own stream drained.
+int quiesce(ck_net* net) {
+  CK_CUDA_TRY(cudaSetDevice(net->device));
+  CK_CUDA_TRY(cudaDeviceSynchronize());
+  return CK_OK;
+}
+
 int run_single(ck_net* net, Job job) {
   CK_CUDA_TRY(cudaSetDevice(net->device));
   job.loss_total = net->d_loss;
@@ -824,6 +835,7 @@ int ck_net_num_params(const ck_net* net, int64_t* n) {
 int ck_net_set_params(ck_net* net, const float* host, int64_t n) {
   CK_CHECK(net && host, CK_E_CONFIG, "null argument");
   CK_CHECK(n == net->n_params, CK_E_DIMENSION, "parameter count mismatch");
+  { const int q = quiesce(net); if (q) return q; }
   CK_CUDA_TRY(cudaSetDevice(net->device));
   CK_CUDA_TRY(cudaMemcpy(net->d_params, host, sizeof(float) * n, cudaMemcpyHostToDevice));
   return CK_OK;
@@ -838,6 +850,7 @@ int ck_net_device_params(const ck_net* net, const float** params) {
 int ck_net_get_params(ck_net* net, float* host, int64_t n) {
   CK_CHECK(net && host, CK_E_CONFIG, "null argument");
   CK_CHECK(n == net->n_params, CK_E_DIMENSION, "parameter count mismatch");
+  { const int q = quiesce(net); if (q) return q; }
   CK_CUDA_TRY(cudaSetDevice(net->device));
   CK_CUDA_TRY(cudaMemcpy(host, net->d_params, sizeof(float) * n, cudaMemcpyDeviceToHost));
   return CK_OK;
@@ -852,6 +865,7 @@ static int stage_input(ck_net* net, const float* x) {
 
 int ck_net_forward(ck_net* net, const float* x, float* y_out) {
   CK_CHECK(net && x, CK_E_CONFIG, "null argument");
+  { const int q = quiesce(net); if (q) return q; }
   CK_CUDA_TRY(cudaSetDevice(net->device));
   int rc = stage_input(net, x);
   if (rc) return rc;
@@ -868,6 +882,7 @@ int ck_net_forward(ck_net* net, const float* x, float* y_out) {
 
 int ck_net_backward(ck_net* net, const double* targets) {
   CK_CHECK(net && targets, CK_E_CONFIG, "null argument");
+  { const int q = quiesce(net); if (q) return q; }
   CK_CUDA_TRY(cudaSetDevice(net->device));
   CK_CUDA_TRY(cudaMemcpyAsync(net->d_targets, targets, sizeof(double) * net->h.n_classes,
                               cudaMemcpyHostToDevice, net->stream));
@@ -879,6 +894,7 @@ int ck_net_backward(ck_net* net, const double* targets) {
 int ck_net_apply_gradients(ck_net* net, double eta) {
   CK_CHECK(net, CK_E_CONFIG, "null net");
   CK_CHECK(eta > 0, CK_E_CONFIG, "learning rate must be > 0");
+  { const int q = quiesce(net); if (q) return q; }
   Job job = empty_job(PROG_APPLY);
   job.eta_f = (float)eta;
   return run_single(net, job);
@@ -887,6 +903,7 @@ int ck_net_apply_gradients(ck_net* net, double eta) {
 int ck_net_train_step(ck_net* net, const float* x, const double* targets, double eta,
                       double* loss) {
   CK_CHECK(net && x && targets, CK_E_CONFIG, "null argument");
+  { const int q = quiesce(net); if (q) return q; }
   CK_CUDA_TRY(cudaSetDevice(net->device));
   int rc = stage_input(net, x);
   if (rc) return rc;
@@ -933,6 +950,7 @@ int ck_net_read_buffer(ck_net* net, int layer, int which, void* host, int64_t co
   int64_t n = 0;
   int rc = ck_net_buffer_size(net, layer, which, &n);
   if (rc) return rc;
+  { const int q = quiesce(net); if (q) return q; }
   CK_CHECK(host && count == n, CK_E_DIMENSION, "buffer size mismatch");
   CK_CUDA_TRY(cudaSetDevice(net->device));
   const LayerDev& L = net->h.L[layer];

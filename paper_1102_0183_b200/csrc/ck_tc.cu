@@ -595,6 +595,15 @@ static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int k
   const int by_regs = g.bk == 64 ? 3 : 4;
   st.ctas_per_sm = std::max(1, std::min(occ(st.smem), by_regs));
   CK_CHECK(st.smem <= 220 * 1024, CK_E_DIMENSION, "tensor-core eval: tile exceeds shared memory");
+  // The block scheduler only sees registers and shared memory: with the
+  // launch bounds' register caps more CTAs than TMEM holds (512 / cols) could
+  // co-reside and spin in tcgen05.alloc.  Pad the dynamic shared memory so
+  // that shared memory alone caps residency at the TMEM limit.
+  {
+    const int tmem_limit = 512 / cols;
+    const size_t need = (size_t)(228 * 1024) / (tmem_limit + 1) - 1024 + 128;
+    if (tmem_limit < by_regs && st.smem < need) st.smem = need;
+  }
   std::vector<int> kdec(g.K_pad, -1);
   for (int k = 0; k < g.K; ++k) {
     const int dec = kdec_host_in[k];

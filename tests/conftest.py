@@ -40,3 +40,21 @@ def golden():
 def _built_oracle():
     from oracle import oracle
     oracle.lib()
+
+
+def reference_convkit():
+    """The reference package (baseline/_ref, else /root/reference in the build
+    container) for side-by-side interface checks; None where it is absent."""
+    import importlib
+    import tempfile
+    for path in (os.path.join(ROOT, "baseline", "_ref"),
+                 os.path.join("/root", "reference", "pkg", "src")):
+        if os.path.isdir(os.path.join(path, "convkit")):
+            if path not in sys.path:
+                sys.path.append(path)
+            os.environ.setdefault("NUMBA_CACHE_DIR", tempfile.mkdtemp(prefix="ck_numba_"))
+            try:
+                return importlib.import_module("convkit")
+            except Exception:
+                return None
+    return None

@@ -136,3 +136,38 @@ def test_train_log_byte_identical(tmp_path, tag, arch, extra):
                           "--weights", os.path.join(G, "plain.weights.npz")])
         assert code == 0 and text == golden_text("plain.eval.txt")
 
+
+
+@pytest.mark.parametrize("tag,arch,extra", [
+    ("plain", "plain.net", []),
+    ("runs2", "plain.net", ["--runs", "2", "--epochs", "2"]),
+    ("deform", "deform.net", []),
+])
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_reference_frontend_over_b200_engine(tmp_path, tag, arch, extra):
+    """SURVEY §8(f)2 backend switch: the reference's unchanged convkit.cli
+    (from baseline/_ref) with its engine symbols rebound to this package
+    reproduces its own transcripts byte for byte."""
+    from tests.conftest import reference_convkit
+    if reference_convkit() is None:
+        pytest.skip("reference package not available")
+    out = tmp_path / tag
+    code, _ = run(["--reference-frontend", "train", "--arch", os.path.join(G, arch),
+                   "--data", G, "--seed", "3", "--no-timing", "--out", str(out), *extra])
+    assert code == 0
+    assert (out / "metrics.log").read_text() == golden_text(f"{tag}.metrics.log")
+    if tag == "plain":
+        code, text = run(["--reference-frontend", "eval", "--arch", os.path.join(G, arch),
+                          "--data", G, "--weights", os.path.join(G, "plain.weights.npz")])
+        assert code == 0 and text == golden_text("plain.eval.txt")
+
+
+def test_reference_frontend_exit_codes():
+    from tests.conftest import reference_convkit
+    if reference_convkit() is None:
+        pytest.skip("reference package not available")
+    assert run(["--reference-frontend", "inspect", "--arch", "/nonexistent.net"])[0] == \
+        cli.EXIT_CONFIG
+    code, text = run(["--reference-frontend", "inspect", "--arch", os.path.join(G, "deform.net")])
+    assert code == 0 and text == golden_text("deform.inspect.txt")
