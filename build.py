@@ -13,7 +13,6 @@ import os
 import shutil
 import subprocess
 import sys
-import tempfile
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_1102_0183_b200")
@@ -56,25 +55,37 @@ def _spec_units() -> list[str]:
                   if f.startswith("ck_spec_") and f.endswith(".cu"))
 
 
+OBJ_DIR = os.path.join(ROOT, "build", "obj")
+
+
 def _compile(out: str, verbose: bool, extra=(), specs: bool = True) -> None:
-    """Every translation unit to an object in parallel, then one link."""
+    """Every translation unit to an object in parallel, then one link.
+    Objects are cached under build/obj (per flag set) and recompiled only when
+    the unit or a shared header changed."""
     units = [os.path.join(CSRC, s) for s in SOURCES] + (_spec_units() if specs else [])
-    tmp = tempfile.mkdtemp(prefix="ckb200_build_")
-    try:
-        procs = []
-        for u in units:
-            obj = os.path.join(tmp, os.path.basename(u) + ".o")
-            cmd = [_nvcc(), *COMPILE_FLAGS, *extra, *UNIT_FLAGS.get(os.path.basename(u), []),
-                   "-c", "-o", obj, u]
-            if verbose:
-                cmd.insert(1, "-Xptxas=-v")
-            procs.append((obj, subprocess.Popen(cmd)))
-        for obj, p in procs:
-            if p.wait() != 0:
-                raise subprocess.CalledProcessError(p.returncode, "nvcc")
-        subprocess.run([_nvcc(), *LINK_FLAGS, "-o", out, *[o for o, _ in procs]], check=True)
-    finally:
-        shutil.rmtree(tmp, ignore_errors=True)
+    headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include",
+                                                                      "ckb200.h")]
+    tag = "stage1" if "-DCK_NO_SPECS" in extra else "full"
+    odir = os.path.join(OBJ_DIR, tag)
+    os.makedirs(odir, exist_ok=True)
+    procs = []
+    objs = []
+    for u in units:
+        obj = os.path.join(odir, os.path.basename(u) + ".o")
+        objs.append(obj)
+        if not verbose and not _stale(obj, [u, *headers, __file__]):
+            continue
+        cmd = [_nvcc(), *COMPILE_FLAGS, *extra, *UNIT_FLAGS.get(os.path.basename(u), []),
+               "-c", "-o", obj, u]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        procs.append((obj, subprocess.Popen(cmd)))
+    for obj, p in procs:
+        if p.wait() != 0:
+            if os.path.exists(obj):
+                os.remove(obj)
+            raise subprocess.CalledProcessError(p.returncode, "nvcc")
+    subprocess.run([_nvcc(), *LINK_FLAGS, "-o", out, *objs], check=True)
 
 
 def generate_specs(lib: str) -> bool:

@@ -13,6 +13,8 @@ into a float32 (n, C, H, W) buffer the training kernel reads directly.
 
 from __future__ import annotations
 
+import dataclasses
+
 import ctypes as C
 from dataclasses import dataclass
 
@@ -148,6 +150,9 @@ def deform_epoch(dd, config: DeformationConfig, seed: int, epoch: int, out=None,
     dev = torch.device("cuda", dd.device)
     if out is None:
         out = torch.empty((n, c, h, w), dtype=torch.float32, device=dev)
+    if not isinstance(config, DeformationConfig):   # e.g. convkit's (same fields)
+        config = DeformationConfig(**{f.name: getattr(config, f.name)
+                                      for f in dataclasses.fields(DeformationConfig)})
     taps, radius = _Taps.get(config.elastic_sigma if config.elastic_sigma > 0 else 1.0,
                              dd.device)
     cfg = config.c_struct()

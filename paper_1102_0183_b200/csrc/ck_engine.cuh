@@ -49,6 +49,7 @@ enum LayerKind { L_INPUT = 0, L_IMGPROC = 1, L_CONV = 2, L_POOL = 3, L_FC = 4 };
   X(int, n_pairs) X(int, has_delta) X(int, n_filt) X(int, fh) X(int, fw)     \
   X(int, max_fan_in) X(int, pool_above)                                      \
   X(int, wg_split) X(int, pull_g) X(int, pull_ch) X(int, full)               \
+  X(int, spitch) X(int, ypitch) X(int64_t, yp_off) X(int, pullg)             \
   X(int64_t, p_off) X(int64_t, b_off) X(int64_t, n_par)                      \
   X(int64_t, y_off) X(int64_t, a_off) X(int64_t, d_off) X(int64_t, arg_off)  \
   X(int64_t, wrc_off) X(int64_t, wd_off)                                     \
@@ -519,6 +520,86 @@ __device__ __forceinline__ float conv_cell_smem(float acc, const float* src, con
   return acc;
 }
 
+// conv_cell_smem with each pair's kx*ky weights at a 16-byte aligned stride of
+// KKP = round_up(kx*ky, 4) floats: a warp (one dest map, or two) reads them
+// as broadcast ld.shared.v4 -- 4x fewer shared-memory wavefronts for the
+// weights, which with the source loads bound the chain's step rate.  Same
+// operands, same order: bit-identical to conv_cell.
+__device__ __forceinline__ float4 lds_v4(unsigned addr) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
+// One source of conv_cell_smem4: rows v = 0..KY-1 with the row ring resolved
+// at compile time (PAR = parity of the source's first row), the next row
+// loaded while the current one is added; `nsrc` is the next source's base.
+template <int KX, int KY, int PAR>
+__device__ __forceinline__ void conv_rows_smem(float& acc, const float* wcur, unsigned sb,
+                                               unsigned nsrc, int sw, float (&xa)[KX],
+                                               float (&xb)[KX]) {
+#pragma unroll
+  for (int v = 0; v < KY; ++v) {
+    const bool cur_a = ((PAR + v) & 1) == 0;
+    const unsigned nrow = v + 1 < KY ? sb + 4u * (unsigned)((v + 1) * sw) : nsrc;
+#pragma unroll
+    for (int u = 0; u < KX; ++u) {
+      if (cur_a) xb[u] = lds_f32(nrow + 4u * u);
+      else xa[u] = lds_f32(nrow + 4u * u);
+    }
+#pragma unroll
+    for (int u = 0; u < KX; ++u)
+      acc = __fadd_rn(acc, __fmul_rn(wcur[v * KX + u], cur_a ? xa[u] : xb[u]));
+  }
+}
+
+template <int KKP>
+__device__ __forceinline__ void lds_weights(float (&w)[KKP], unsigned addr) {
+#pragma unroll
+  for (int j = 0; j < KKP / 4; ++j) {
+    const float4 v = lds_v4(addr + 16u * j);
+    w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+  }
+}
+
+// The reference-order chain of one conv cell with every operand in shared
+// memory: each pair's kx*ky weights at a 16-byte aligned stride of KKP =
+// round_up(kx*ky, 4) floats, read as broadcast ld.shared.v4 a whole source
+// ahead; source rows one row ahead.  Two sources per loop iteration resolve
+// both register rings (rows, weights) at compile time, so no register copies
+// reach the FMA pipe: per tap it issues exactly the FMUL and the FADD (2
+// cycles each per warp -- with the 4-cycle FADD latency, the chain's floor;
+// tools/mb_conv.cu V12).  Same operands, same order: bit-identical to
+// conv_cell.
+template <int KX, int KY>
+__device__ __forceinline__ float conv_cell_smem4(float acc, const float* src, const int* soff,
+                                                 const float* w, int nk, int sw) {
+  constexpr int KK = KX * KY, KKP = (KK + 3) & ~3;
+  (void)KK;
+  const unsigned s0 = (unsigned)__cvta_generic_to_shared(src);
+  const unsigned o0 = (unsigned)__cvta_generic_to_shared(soff);
+  const unsigned w0 = (unsigned)__cvta_generic_to_shared(w);
+  float xa[KX], xb[KX], wa[KKP], wb[KKP];
+  lds_weights<KKP>(wa, w0);
+  unsigned sb = s0 + 4u * (unsigned)lds_s32(o0);
+#pragma unroll
+  for (int u = 0; u < KX; ++u) xa[u] = lds_f32(sb + 4u * u);
+  int k = 0;
+  for (; k + 2 <= nk; k += 2) {
+    const unsigned sb1 = s0 + 4u * (unsigned)lds_s32(o0 + 4u * (k + 1));
+    lds_weights<KKP>(wb, w0 + 4u * (unsigned)((k + 1) * KKP));
+    conv_rows_smem<KX, KY, 0>(acc, wa, sb, sb1, sw, xa, xb);
+    const int k2 = k + 2 < nk ? k + 2 : k + 1;
+    const unsigned sb2 = s0 + 4u * (unsigned)lds_s32(o0 + 4u * k2);
+    lds_weights<KKP>(wa, w0 + 4u * (unsigned)(k2 * KKP));
+    conv_rows_smem<KX, KY, KY & 1>(acc, wb, sb1, sb2, sw, xa, xb);
+    sb = sb2;
+  }
+  if (k < nk) conv_rows_smem<KX, KY, 0>(acc, wa, sb, sb, sw, xa, xb);
+  return acc;
+}
+
 // All PB x PB conv cells of one pool block, one thread: the block shares its
 // dest map's weights (one load per tap for PB*PB chains) and its source
 // window (loads shared between neighbouring cells).  Each cell's own chain
@@ -621,6 +702,15 @@ __device__ __forceinline__ void op_conv_fwd(const NetGeo& N, const NetPtr& R, co
   else conv_fwd_chunk<0, 0>(N, R, L, flags, act, tm);
 }
 
+// A pooled value, plus its pre-pitched copy when the consumer asked for one.
+__device__ __forceinline__ void store_pooled(const LayerDev& P, float* act, int q, float v) {
+  act[P.y_off + q] = v;
+  if (P.ypitch > 0) {
+    const int phw = P.h * P.w, m = q / phw, pix = q - m * phw, r = pix / P.w;
+    act[P.yp_off + (int64_t)(m * P.h + r) * P.ypitch + (pix - r * P.w)] = v;
+  }
+}
+
 // max-pool (kernels.py:154-172): strict '>' keeps the first cell in scan order.
 // The argmax is stored as an index into the whole source layer.
 __device__ __forceinline__ void op_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
@@ -644,7 +734,7 @@ __device__ __forceinline__ void op_pool_fwd(const NetGeo& N, const NetPtr& R, co
         const float val = src[i];
         if (val > best) { best = val; best_i = i; }
       }
-    y[q] = best;
+    store_pooled(L, act, q, best);
     arg[q] = best_i;
     if (S.kind == L_CONV) {
       const int local = best_i - base;
@@ -699,6 +789,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
   int used = 0;
   const float* src_g = act + S.y_off;
   const float* src = src_g;
+  int sw = S.w;               // row pitch of `src` (L.spitch when staged pitched)
   if (li == 1) {
     if (sp.b < sp.e) {
       const float* si = stage_input(N, R, tm, used);
@@ -706,12 +797,23 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     }
   } else if (sp.b < sp.e && S.cells <= tm.smem_floats / 2) {
     // the whole source layer, unless this CTA's maps connect to fewer cells
+    // (from the producer's pre-pitched copy -- bank-conflict-free reads --
+    // when it still leaves the chunk 3/8 of the scratch)
     const int nk_all = t_fwd_off(R, L, ((sp.e - 1) / phw + 1)) - t_fwd_off(R, L, (sp.b / phw));
     CK_SUBT(tm, 20);
-    if (S.cells <= nk_all * shw) src = stage(src, S.cells, tm, used);
+    if (S.cells <= nk_all * shw) {
+      if (S.ypitch > 0 && S.maps * S.h * S.ypitch <= tm.smem_floats / 8 * 5) {
+        src = stage(act + S.yp_off, S.maps * S.h * S.ypitch, tm, used);
+        sw = S.ypitch;
+      } else {
+        src = stage(src, S.cells, tm, used);
+      }
+    }
     CK_SUBT(tm, 21);
   }
   const bool whole = src != src_g;
+  const int smap = S.h * sw;  // map stride of `src`
+  constexpr int KKP = KX > 0 ? ((KX * KY + 3) & ~3) : 1;
   const bool zero = full && (flags & F_ZERO_SELF);
   const bool pooled_only = (flags & F_POOLED_ONLY) && !full;
   // The arena is tiled like ConnectionTable (checked at ck_net_create): dest
@@ -728,7 +830,8 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     for (int tries = 0; tries < 24; ++tries) {
       const int d0 = q / phw, d1 = (qe - 1) / phw;
       const int nk = t_fwd_off(R, L, (d1 + 1)) - t_fwd_off(R, L, (d0));
-      const int nw = nk * kk + d1 + 1 - d0;
+      // weights: unpadded, or per pair at a KKP stride plus the biases (chain path)
+      const int nw = nk * (KX > 0 ? KKP : kk) + d1 + 1 - d0;
       const int base = ((nk + 3) & ~3) + ((nw + 3) & ~3) + (qe - q) * blk;
       if (!whole && base + nk * shw <= avail) { wst = slots = true; break; }
       if (whole && base <= avail) { wst = true; break; }
@@ -742,17 +845,35 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     const int d0 = q / phw, d1 = (qe - 1) / phw;
     const int k0 = t_fwd_off(R, L, (d0)), k1 = t_fwd_off(R, L, (d1 + 1));
     const int w0 = k0 * kk + d0;
-    const int nw = (k1 - k0) * kk + d1 + 1 - d0;
+    const int n_items = (qe - q) * blk;
+    // one pool block per thread (many cells per CTA), else one cell per
+    // thread on the reference-order chain with padded (v4) weights
+    const bool block_path = KX > 0 && wst && (whole || slots) && P.px == P.py && P.px >= 2 &&
+                            P.px <= 4 && n_items > 2 * (int)blockDim.x;
+    const bool padw = KX > 0 && wst && (whole || slots) && !block_path;
+    const int nw = (k1 - k0) * (padw ? KKP : kk) + d1 + 1 - d0;
     int* soff = reinterpret_cast<int*>(tm.smem + used);
     float* ws = tm.smem + used + ((k1 - k0 + 3) & ~3);
+    float* bs = ws + (k1 - k0) * KKP;   // padw: the chunk's biases after its blocks
     float* ybuf = wst ? ws + ((nw + 3) & ~3) : tm.smem + used;
     float* sslot = ybuf + (qe - q) * blk;
     const float* sbase = slots ? sslot : src;
     if (wst) {
-      int u2 = used + ((k1 - k0 + 3) & ~3);
-      stage(arena + w0, nw, tm, u2);
+      if (padw) {
+        // pair k0 + j's kk weights (arena index p * kk + dest(p), topology
+        // tiling) at ws + j * KKP; dest d's bias at bs[d - d0]
+        for (int e = threadIdx.x; e < (k1 - k0) * kk; e += blockDim.x) {
+          const int j = e / kk, t = e - j * kk;
+          cp_async4(ws + j * KKP + t, arena + (k0 + j) * kk + t_pair_dst(R, L, k0 + j) + t);
+        }
+        for (int d = d0 + threadIdx.x; d <= d1; d += blockDim.x)
+          cp_async4(bs + (d - d0), arena + t_fwd_off(R, L, d + 1) * kk + d);
+      } else {
+        int u2 = used + ((k1 - k0 + 3) & ~3);
+        stage(arena + w0, nw, tm, u2);
+      }
       for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x)
-        soff[k] = slots ? k * shw : t_fwd_src(R, L, (k0 + k)) * shw;
+        soff[k] = slots ? k * shw : t_fwd_src(R, L, (k0 + k)) * smap;
       if (slots)
         for (int k = (threadIdx.x >> 5); k < k1 - k0; k += (blockDim.x >> 5)) {
           const float* from = src_g + t_fwd_src(R, L, (k0 + k)) * shw;
@@ -762,28 +883,26 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     CK_SUBT(tm, 3);
     stage_sync();
     CK_SUBT(tm, 4);
-    const int n_items = (qe - q) * blk;
     if constexpr (KX > 0) {
       // many cells per thread: one pool block per thread (conv_block_smem)
-      if (wst && (whole || slots) && P.px == P.py && P.px >= 2 && P.px <= 4 &&
-          n_items > 2 * (int)blockDim.x) {
+      if (block_path) {
         for (int qi = threadIdx.x; qi < qe - q; qi += blockDim.x) {
           const int qq = q + qi;
           const int d = qq / phw, pp = qq % phw;
           const int r0 = (pp / P.w) * P.py, c0 = (pp % P.w) * P.px;
           const int kb = t_fwd_off(R, L, d), ke = t_fwd_off(R, L, d + 1);
           const float* w = ws + (kb * kk + d - w0);
-          const float* sp = sbase + (r0 * L.ty) * S.w + c0 * L.tx;
+          const float* sp = sbase + (r0 * L.ty) * sw + c0 * L.tx;
           float acc[16];
           const float bias = w[(ke - kb) * kk];
 #pragma unroll
           for (int t = 0; t < 16; ++t) acc[t] = bias;
           if (P.px == 2)
-            conv_block_smem<KX, KY, 2>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
+            conv_block_smem<KX, KY, 2>(acc, sp, soff + (kb - k0), w, ke - kb, sw, L.ty, L.tx);
           else if (P.px == 3)
-            conv_block_smem<KX, KY, 3>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
+            conv_block_smem<KX, KY, 3>(acc, sp, soff + (kb - k0), w, ke - kb, sw, L.ty, L.tx);
           else
-            conv_block_smem<KX, KY, 4>(acc, sp, soff + (kb - k0), w, ke - kb, S.w, L.ty, L.tx);
+            conv_block_smem<KX, KY, 4>(acc, sp, soff + (kb - k0), w, ke - kb, sw, L.ty, L.tx);
           int bt = 0;
           float best = 0.0f;
           if (pooled_only) {
@@ -801,7 +920,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
             }
           }
           const int r = r0 + bt / P.px, c = c0 + bt % P.px;
-          pyv[qq] = best;
+          store_pooled(P, act, qq, best);
           parg[qq] = d * hw + r * L.w + c;
           pwrc[qq] = (r << 16) | c;
         }
@@ -820,15 +939,15 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
         const int kb = t_fwd_off(R, L, (d)), ke = t_fwd_off(R, L, (d + 1));
         const float* w = ws + (kb * kk + d - w0);
         if constexpr (KX > 0) {
-          if (whole || slots)   // weights, offsets and sources all in shared memory
-            acc = conv_cell_smem<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
-                                         soff + (kb - k0), w, ke - kb, S.w);
+          if (padw)   // weights (v4), offsets and sources all in shared memory
+            acc = conv_cell_smem4<KX, KY>(bs[d - d0], sbase + (r * L.ty) * sw + c * L.tx,
+                                          soff + (kb - k0), ws + (kb - k0) * KKP, ke - kb, sw);
           else
-            acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
-                                    soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+            acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * sw + c * L.tx,
+                                    soff + (kb - k0), w, ke - kb, sw, L.kx, L.ky);
         } else {
-          acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * S.w + c * L.tx,
-                                  soff + (kb - k0), w, ke - kb, S.w, L.kx, L.ky);
+          acc = conv_cell<KX, KY>(w[(ke - kb) * kk], sbase + (r * L.ty) * sw + c * L.tx,
+                                  soff + (kb - k0), w, ke - kb, sw, L.kx, L.ky);
         }
       } else {
         acc = conv_value_global<KX, KY>(R, L, S, arena, src, d, r, c);
@@ -858,7 +977,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
       const int d = qq / phw, pp = qq % phw;
       const int r = (pp / P.w) * P.py + bt / P.px;
       const int c = (pp % P.w) * P.px + bt % P.px;
-      pyv[qq] = best;
+      store_pooled(P, act, qq, best);
       parg[qq] = d * hw + r * L.w + c;
       pwrc[qq] = (r << 16) | c;
     }
@@ -877,7 +996,8 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
         int r, c;
         if (k < strip) { r = k / (L.w - cw); c = cw + k % (L.w - cw); }
         else { r = rh + (k - strip) / L.w; c = (k - strip) % L.w; }
-        const float acc = conv_value_global<KX, KY>(R, L, S, arena, whole ? src : src_g, d, r, c);
+        const float acc = conv_value_global<KX, KY>(R, L, S, arena,
+                                                    whole && sw == S.w ? src : src_g, d, r, c);
         const int cell = d * hw + r * L.w + c;
         a[cell] = acc;
         y[cell] = conv_act(acc);
@@ -1204,6 +1324,155 @@ __device__ __forceinline__ void emit_wg(int o, int t, double sum, double* out, f
   else g[o + t] = (float)sum;
 }
 
+// Pull as a GATHER in the reference's order (kernels.py:90-121): one thread
+// per source cell, one f64 accumulator over the backward list (dests k in
+// list order) and, per dest, the covering conv cells in row, then column
+// order; every term is the f32 product delta * w.  Below a max-pool the conv
+// deltas are zero except at the pool winners (a zero term adds an exact +0),
+// so per dest only the winners of the pooled cells whose blocks meet the
+// covering rectangle [ylo, yhi] x [xlo, xhi] contribute.  Those candidates
+// form a small grid (<= PRM pooled rows x PCM pooled cols, fixed per layer);
+// all their winner loads are issued together (no dependent branch per
+// candidate), and each pooled row's matches are stably sorted by conv row:
+// across pooled rows the winners' rows already ascend, inside one the
+// columns ascend with the pooled column -- so the adds follow the
+// reference's (y, x) order exactly.  Bit-identical to kernels.pull_bwd.
+// Every CTA takes a contiguous range of source cells; the winners of all
+// dest maps and the CTA's backward entries' (old) kernels are staged.
+template <int PRM, int PCM>
+__device__ __forceinline__ void pull_gather_cells(const NetGeo& N, const NetPtr& R,
+                                                  const LayerDev& L, float* act, Span cs,
+                                                  const int* wr, const float* wdv,
+                                                  const float* ws, int ka) {
+  const int li = &L - N.L;
+  const LayerDev& S = N.L[li - 1];
+  const LayerDev& P = N.L[li + 1];
+  const int shw = S.h * S.w, phw = P.h * P.w, kk = L.kx * L.ky;
+  // everything staged: 32-bit shared addresses, ld.shared (no generic loads)
+  const unsigned wr0 = (unsigned)__cvta_generic_to_shared(wr);
+  const unsigned wd0 = (unsigned)__cvta_generic_to_shared(wdv);
+  const unsigned ws0 = (unsigned)__cvta_generic_to_shared(ws);
+  for (int cell = cs.b + threadIdx.x; cell < cs.e; cell += blockDim.x) {
+    const int s = cell / shw, pix = cell - s * shw;
+    const int j = pix / S.w, i = pix - j * S.w;
+    const int ylo = ceil_div_clamp0(j - L.ky + 1, L.ty), yhi = min(j / L.ty, L.h - 1);
+    const int xlo = ceil_div_clamp0(i - L.kx + 1, L.tx), xhi = min(i / L.tx, L.w - 1);
+    const int pr0 = ylo / P.py, pr1 = min(yhi / P.py, P.h - 1);
+    const int pc0 = xlo / P.px, pc1 = min(xhi / P.px, P.w - 1);
+    double acc = 0.0;
+    if (ylo <= yhi && xlo <= xhi && pr0 <= pr1 && pc0 <= pc1) {
+      // candidate pooled cells (dest-independent): byte offsets and validity
+      unsigned qo[PRM][PCM];
+      bool qv[PRM][PCM];
+#pragma unroll
+      for (int a = 0; a < PRM; ++a)
+#pragma unroll
+        for (int b = 0; b < PCM; ++b) {
+          qv[a][b] = pr0 + a <= pr1 && pc0 + b <= pc1;
+          qo[a][b] = 4u * (unsigned)(min(pr0 + a, pr1) * P.w + min(pc0 + b, pc1));
+        }
+      const int e0 = t_bwd_off(R, L, s), e1 = t_bwd_off(R, L, s + 1);
+      const int tap0 = j * L.kx + i;     // tap = tap0 - r*ty*kx - c*tx
+#pragma unroll 2
+      for (int e = e0; e < e1; ++e) {
+        const int d = t_bwd_dst(R, L, e);
+        const unsigned wrd = wr0 + 4u * (unsigned)(d * phw);
+        const unsigned wdd = wd0 + 4u * (unsigned)(d * phw);
+        const unsigned wb = ws0 + 4u * (unsigned)((e - ka) * kk);
+        int key[PRM][PCM];
+        double term[PRM][PCM];
+#pragma unroll
+        for (int a = 0; a < PRM; ++a)
+#pragma unroll
+          for (int b = 0; b < PCM; ++b) {
+            const int rc = lds_s32(wrd + qo[a][b]);
+            const float dv = lds_f32(wdd + qo[a][b]);
+            const int r = rc >> 16, c = rc & 0xffff;
+            const bool ok = qv[a][b] && r >= ylo && r <= yhi && c >= xlo && c <= xhi;
+            const int tap = ok ? tap0 - r * L.ty * L.kx - c * L.tx : 0;
+            const float prod = __fmul_rn(dv, lds_f32(wb + 4u * (unsigned)tap));
+            key[a][b] = ok ? r : 0x7fffffff;
+            term[a][b] = ok ? (double)prod : 0.0;
+          }
+#pragma unroll
+        for (int a = 0; a < PRM; ++a) {
+          // stable sort of the pooled row's matches by conv row (bubble network)
+#pragma unroll
+          for (int pass = 0; pass < PCM - 1; ++pass)
+#pragma unroll
+            for (int b = 0; b + 1 < PCM - pass; ++b) {
+              const bool sw = key[a][b] > key[a][b + 1];
+              const int k0 = key[a][b], k1 = key[a][b + 1];
+              const double t0 = term[a][b], t1 = term[a][b + 1];
+              key[a][b] = sw ? k1 : k0;
+              key[a][b + 1] = sw ? k0 : k1;
+              term[a][b] = sw ? t1 : t0;
+              term[a][b + 1] = sw ? t0 : t1;
+            }
+#pragma unroll
+          for (int b = 0; b < PCM; ++b)
+            if (key[a][b] != 0x7fffffff) acc += term[a][b];
+        }
+      }
+    }
+    emit_delta(N, R, act, li - 1, cell, (float)acc);
+  }
+}
+
+// The candidate grid spans at most ceil((ky-1)/ty/py)+1 pooled rows (cols
+// likewise); layers beyond 5x5 candidates keep the scatter (host flag).
+__device__ __forceinline__ void conv_pull_gather(const NetGeo& N, const NetPtr& R,
+                                                 const LayerDev& L, float* act,
+                                                 const TeamCtx& tm) {
+  const int li = &L - N.L;
+  const LayerDev& S = N.L[li - 1];
+  const LayerDev& P = N.L[li + 1];
+  const int shw = S.h * S.w, phw = P.h * P.w, kk = L.kx * L.ky;
+  const float* arena = R.params + L.p_off;
+  const Span cs = cta_span(S.cells, tm);
+  if (cs.b >= cs.e) return;                      // uniform per CTA
+  CK_SUBT(tm, 16);
+  const int nwin = L.maps * phw;
+  // the host sets pullg only when the winners of all dest maps and any CTA's
+  // backward-entry kernels fit the scratch (ck_net.cu); chunks of cells keep
+  // the kernels' share bounded for wide backward lists
+  int used = 0;
+  const int* wr = reinterpret_cast<const int*>(
+      stage(reinterpret_cast<const float*>(act + P.wrc_off), nwin, tm, used));
+  const float* wdv = stage(act + P.wd_off, nwin, tm, used);
+  float* ws = tm.smem + used;
+  const int cap = tm.smem_floats - used;
+  const int prm = ((L.ky - 1) / L.ty + P.py - 1) / P.py + 1;
+  const int pcm = ((L.kx - 1) / L.tx + P.px - 1) / P.px + 1;
+  for (int c0 = cs.b; c0 < cs.e;) {
+    // cells [c0, c1): whole source maps' backward entries must fit
+    int c1 = cs.e;
+    int m0 = c0 / shw, m1 = (c1 - 1) / shw;
+    int ka = t_bwd_off(R, L, m0), kb = t_bwd_off(R, L, m1 + 1);
+    while ((kb - ka) * kk > cap && m1 > m0) {
+      c1 = m1 * shw;
+      m1 = (c1 - 1) / shw;
+      kb = t_bwd_off(R, L, m1 + 1);
+    }
+    if (c0 != cs.b) __syncthreads();             // previous chunk's kernels consumed
+    for (int e = threadIdx.x; e < (kb - ka) * kk; e += blockDim.x) {
+      const int q = e / kk;
+      cp_async4(ws + e, arena + t_bwd_widx(R, L, ka + q) + (e - q * kk));
+    }
+    stage_sync();
+    CK_SUBT(tm, 17);
+    const Span ch{c0, c1};
+    if (prm <= 1 && pcm <= 1) pull_gather_cells<1, 1>(N, R, L, act, ch, wr, wdv, ws, ka);
+    else if (prm <= 2 && pcm <= 2) pull_gather_cells<2, 2>(N, R, L, act, ch, wr, wdv, ws, ka);
+    else if (prm <= 3 && pcm <= 3) pull_gather_cells<3, 3>(N, R, L, act, ch, wr, wdv, ws, ka);
+    else pull_gather_cells<5, 5>(N, R, L, act, ch, wr, wdv, ws, ka);
+    c0 = c1;
+  }
+  CK_SUBT(tm, 18);
+  __syncthreads();
+  CK_SUBT(tm, 19);
+}
+
 // Each CTA stages exactly what its share needs (one cp.async round trip per
 // chunk), then computes from shared memory:
 //   weight_grad  its pairs [p0, p1): the winners of their dest maps and one
@@ -1235,7 +1504,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   // (one per CTA) those CTAs take no weight-gradient work, which the other
   // ranks share.  Every sum keeps its fixed order, so results do not depend
   // on the split.
-  const int npull = ((flags & F_PULL) && 2 * S.maps <= tm.size) ? S.maps : 0;
+  const int npull = ((flags & F_PULL) && !L.pullg && 2 * S.maps <= tm.size) ? S.maps : 0;
   const int wg_ranks = tm.size - npull;
 
   // ---- weight gradients
@@ -1332,6 +1601,11 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   CK_SUBT(tm, 15);
   if (!(flags & F_PULL)) {
     __syncthreads();
+    return;
+  }
+  if (L.pullg) {
+    __syncthreads();
+    conv_pull_gather(N, R, L, act, tm);
     return;
   }
 

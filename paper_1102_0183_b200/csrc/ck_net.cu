@@ -393,6 +393,52 @@ int run_single(ck_net* net, Job job) {
   return CK_OK;
 }
 
+// Row pitch for a conv's source layer staged whole in shared memory
+// (conv_pool_fwd): the lanes of a warp take consecutive cells of pool blocks
+// (one cell each, reference-order chain) and at every step all read the same
+// tap of their own window; the pitch decides which banks those addresses hit.
+// Pick the smallest pitch in [w, w + 32) minimising the shared-memory
+// wavefronts of one such load, summed over the warps of a 148-CTA team.
+// Performance only: every pitch gives the same bits.
+static int choose_src_pitch(const LayerDev& L, const LayerDev& S, const LayerDev& P) {
+  const int blk = P.px * P.py, phw = P.h * P.w, team = 148;
+  int best_pitch = S.w;
+  long best = -1;
+  for (int pitch = S.w; pitch < S.w + 32; ++pitch) {
+    long total = 0;
+    for (int rank = 0; rank < team; ++rank) {
+      const int qb = (int)((int64_t)P.cells * rank / team);
+      const int qe = (int)((int64_t)P.cells * (rank + 1) / team);
+      const int items = (qe - qb) * blk;
+      for (int w0 = 0; w0 < items; w0 += 32) {
+        int addr[32], n = 0;
+        for (int it = w0; it < std::min(items, w0 + 32); ++it) {
+          const int pp = (qb + it / blk) % phw, t = it % blk;
+          const int r = (pp / P.w) * P.py + t / P.px, c = (pp % P.w) * P.px + t % P.px;
+          addr[n++] = r * L.ty * pitch + c * L.tx;
+        }
+        int worst = 0;
+        for (int bank = 0; bank < 32; ++bank) {
+          int distinct = 0;
+          for (int i = 0; i < n; ++i) {
+            if (addr[i] % 32 != bank) continue;
+            bool seen = false;
+            for (int j = 0; j < i; ++j) seen = seen || addr[j] == addr[i];
+            distinct += seen ? 0 : 1;
+          }
+          worst = std::max(worst, distinct);
+        }
+        total += worst;
+      }
+    }
+    if (best < 0 || total < best) {
+      best = total;
+      best_pitch = pitch;
+    }
+  }
+  return best_pitch;
+}
+
 // The whole device description of a net from its resolved layers -- pure
 // host code (no CUDA calls), shared by ck_net_create and the spec generator.
 int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
@@ -452,6 +498,15 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
         // the backward list, <= 16 f64 copies of a source map in shared memory
         C.pull_g = kk >= 32 ? 1 : std::min(32 / kk, phw);
         C.pull_ch = std::max(1, 16 / C.pull_g);
+        // the pull as a bit-exact gather (conv_pull_gather); CKB200_PULL=scatter: A/B
+        {
+          const char* pm = getenv("CKB200_PULL");
+          const int prm = ((C.ky - 1) / C.ty + D.py - 1) / D.py + 1;
+          const int pcm = ((C.kx - 1) / C.tx + D.px - 1) / D.px + 1;
+          // staged: every dest map's winners + one source map's backward
+          // kernels at a time (re-checked with the tables below); else the scatter
+          C.pullg = (pm && strcmp(pm, "scatter") == 0) || prm > 5 || pcm > 5 ? 0 : 1;
+        }
         const int src_cells = N.L[k - 2].h * N.L[k - 2].w;
         while (C.pull_ch > 1 && C.pull_ch * C.pull_g * src_cells * 2 > kTeamStageFloats / 2)
           --C.pull_ch;
@@ -528,6 +583,17 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
   if (N.n_classes > kScratchDoubles) {
     return set_error(CK_E_CONFIG, "too many output classes");
   }
+  // pre-pitched copies of pool outputs a conv+pool consumes (conv_pool_fwd)
+  for (int k = 2; k + 1 < n_layers && !getenv("CKB200_NO_PITCH"); ++k) {   // A/B switch
+    LayerDev& S = N.L[k - 1];
+    if (N.L[k].kind != L_CONV || N.L[k + 1].kind != L_POOL || S.kind != L_POOL) continue;
+    const int pitch = choose_src_pitch(N.L[k], S, N.L[k + 1]);
+    if (pitch <= S.w) continue;
+    N.L[k].spitch = pitch;
+    S.ypitch = pitch;
+    S.yp_off = a_cursor;
+    a_cursor = align32(a_cursor + (int64_t)S.maps * S.h * pitch);
+  }
   N.act_size = a_cursor;
   *n_params = p_cursor;
 
@@ -587,6 +653,19 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
       for (int p = 0; full && p < D.n_pairs; ++p)
         full = fwd_src[p] == p % n_src && pair_dst[p] == p / n_src;
       N.L[k].full = full ? 1 : 0;
+    }
+    // gather pull: measured faster than the stream scatter only for very wide
+    // backward lists (C4': 300 dests per source, 399 -> 156 us per image in
+    // the pull phase; C1-C4 are faster with the scatter) -- and it needs all
+    // winners + the widest source's backward kernels staged
+    if (k + 1 < n_layers && N.L[k].pullg) {
+      const int phw = N.L[k + 1].h * N.L[k + 1].w;
+      const int widest = *std::max_element(count.begin(), count.end());
+      const char* pm = getenv("CKB200_PULL");
+      const bool forced = pm && strcmp(pm, "gather") == 0;
+      if ((widest < 128 && !forced) ||
+          2 * ((L.maps * phw + 3) & ~3) + widest * D.kx * D.ky > kTeamStageFloats)
+        N.L[k].pullg = 0;
     }
     // backward CSR = exact transpose, destinations ascending (topology.invert_table)
     bwd_off[0] = 0;

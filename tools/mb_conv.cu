@@ -210,6 +210,234 @@ __device__ __forceinline__ void cell_v6(float acc, const float* src, const int* 
   o[0] = a0; o[1] = a1;
 }
 
+// V7: the engine's conv_cell_smem4 (rows of x one row ahead, v4 weights a
+// source ahead, 28-float padded weight blocks)
+__device__ __forceinline__ float cell_v7(float acc, const float* src, const int* soff,
+                                         const float* w28) {
+  constexpr int KKP = 28;
+  float wc[KKP], xr[KX];
+  const float* sb = src + soff[0];
+  for (int j = 0; j < 7; ++j) {
+    const float4 v = reinterpret_cast<const float4*>(w28)[j];
+    wc[4 * j] = v.x; wc[4 * j + 1] = v.y; wc[4 * j + 2] = v.z; wc[4 * j + 3] = v.w;
+  }
+#pragma unroll
+  for (int u = 0; u < KX; ++u) xr[u] = sb[u];
+  for (int k = 0; k < NK; ++k) {
+    const int kn = k + 1 < NK ? k + 1 : k;
+    const float* sbn = src + soff[kn];
+    float wn[KKP];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+      const float4 v = reinterpret_cast<const float4*>(w28 + kn * KKP)[j];
+      wn[4 * j] = v.x; wn[4 * j + 1] = v.y; wn[4 * j + 2] = v.z; wn[4 * j + 3] = v.w;
+    }
+#pragma unroll
+    for (int v = 0; v < KY; ++v) {
+      const float* nrow = v + 1 < KY ? sb + (v + 1) * SW : sbn;
+      float xn[KX];
+#pragma unroll
+      for (int u = 0; u < KX; ++u) xn[u] = nrow[u];
+#pragma unroll
+      for (int u = 0; u < KX; ++u) acc = __fadd_rn(acc, __fmul_rn(wc[v * KX + u], xr[u]));
+#pragma unroll
+      for (int u = 0; u < KX; ++u) xr[u] = xn[u];
+    }
+#pragma unroll
+    for (int t = 0; t < KKP; ++t) wc[t] = wn[t];
+    sb = sbn;
+  }
+  return acc;
+}
+
+// V8: pure dependent chain from registers (latency floor reference)
+__device__ __forceinline__ float cell_v8(float acc, const float* src, const int* soff,
+                                         const float* w) {
+  float wr[KK], xr[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) { wr[t] = w[t]; xr[t] = src[(t / KX) * SW + t % KX]; }
+  for (int k = 0; k < NK; ++k) {
+#pragma unroll
+    for (int t = 0; t < KK; ++t) acc = __fadd_rn(acc, __fmul_rn(wr[t], xr[t]));
+  }
+  return acc;
+}
+
+// V9: V8 plus one independent shared load per step (issue cost of the LDS)
+__device__ __forceinline__ float cell_v9(float acc, const float* src, const int* soff,
+                                         const float* w) {
+  float wr[KK], xr[KK];
+  int junk = 0;
+#pragma unroll
+  for (int t = 0; t < KK; ++t) { wr[t] = w[t]; xr[t] = src[(t / KX) * SW + t % KX]; }
+  for (int k = 0; k < NK; ++k) {
+    const float* s = src + soff[k];
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      junk ^= __float_as_int(s[(t / KX) * SW + t % KX]);
+      acc = __fadd_rn(acc, __fmul_rn(wr[t], xr[t]));
+    }
+  }
+  return acc + (junk == 12345 ? 1.0f : 0.0f);
+}
+
+// V10: x of the next source loaded a whole source ahead (double buffer),
+// weights held in registers (timing stand-in: same weights every source)
+__device__ __forceinline__ float cell_v10(float acc, const float* src, const int* soff,
+                                          const float* w) {
+  float wr[KK], xc[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) { wr[t] = w[t]; xc[t] = src[(t / KX) * SW + t % KX]; }
+  for (int k = 0; k < NK; ++k) {
+    const int kn = k + 1 < NK ? k + 1 : k;
+    const float* s = src + soff[kn];
+    float xn[KK];
+#pragma unroll
+    for (int t = 0; t < KK; ++t) xn[t] = s[(t / KX) * SW + t % KX];
+#pragma unroll
+    for (int t = 0; t < KK; ++t) acc = __fadd_rn(acc, __fmul_rn(wr[t], xc[t]));
+#pragma unroll
+    for (int t = 0; t < KK; ++t) xc[t] = xn[t];
+  }
+  return acc;
+}
+
+// V11: FADD-only chain from registers (no FMUL): the add latency alone
+__device__ __forceinline__ float cell_v11(float acc, const float* src, const int* soff,
+                                          const float* w) {
+  float pr[KK];
+#pragma unroll
+  for (int t = 0; t < KK; ++t) pr[t] = w[t] * src[(t / KX) * SW + t % KX];
+  for (int k = 0; k < NK; ++k) {
+#pragma unroll
+    for (int t = 0; t < KK; ++t) acc = __fadd_rn(acc, pr[t]);
+  }
+  return acc;
+}
+
+// V12: no register copies -- the row ring and the weight ring are resolved
+// at compile time (two sources per loop iteration), so the FMA pipe sees
+// exactly FMUL + FADD per tap (rt 2 cycles each: the 4-cycle floor)
+template <int P>
+__device__ __forceinline__ void v12_rows(float& acc, const float* wcur, const float* sb,
+                                         const float* nsrc, float (&xa)[KX], float (&xb)[KX]) {
+#pragma unroll
+  for (int v = 0; v < KY; ++v) {
+    const bool cur_a = ((P + v) & 1) == 0;
+    const float* nrow = v + 1 < KY ? sb + (v + 1) * SW : nsrc;
+#pragma unroll
+    for (int u = 0; u < KX; ++u) {
+      if (cur_a) xb[u] = nrow[u]; else xa[u] = nrow[u];
+    }
+#pragma unroll
+    for (int u = 0; u < KX; ++u)
+      acc = __fadd_rn(acc, __fmul_rn(wcur[v * KX + u], cur_a ? xa[u] : xb[u]));
+  }
+}
+__device__ __forceinline__ void v12_w(float (&wd)[28], const float* w28, int k) {
+#pragma unroll
+  for (int j = 0; j < 7; ++j) {
+    const float4 v = reinterpret_cast<const float4*>(w28 + k * 28)[j];
+    wd[4 * j] = v.x; wd[4 * j + 1] = v.y; wd[4 * j + 2] = v.z; wd[4 * j + 3] = v.w;
+  }
+}
+__device__ __forceinline__ float cell_v12(float acc, const float* src, const int* soff,
+                                          const float* w28) {
+  float xa[KX], xb[KX], wa[28], wb[28];
+  v12_w(wa, w28, 0);
+  const float* sb = src + soff[0];
+#pragma unroll
+  for (int u = 0; u < KX; ++u) xa[u] = sb[u];
+  int k = 0;
+  for (; k + 2 <= NK; k += 2) {
+    const float* sb1 = src + soff[k + 1];
+    v12_w(wb, w28, k + 1);
+    v12_rows<0>(acc, wa, sb, sb1, xa, xb);
+    const int k2 = k + 2 < NK ? k + 2 : k + 1;
+    const float* sb2 = src + soff[k2];
+    v12_w(wa, w28, k2);
+    v12_rows<KY & 1>(acc, wb, sb1, sb2, xa, xb);
+    sb = sb2;
+  }
+  if (k < NK) v12_rows<0>(acc, wa, sb, sb, xa, xb);
+  return acc;
+}
+
+// V13: rows prefetched TWO rows ahead (3-buffer ring), weights a source
+// ahead (2-buffer ring); both rings resolved at compile time by unrolling 6
+// sources per iteration (6*KY rows: divisible by 3 and 2); the tail (< 6
+// sources) reuses the same body under a run-time bound.
+struct Ring3 { float r[3][KX]; };
+template <int G>   // G: sources in this block (compile-time), rows 0..G*KY-1
+__device__ __forceinline__ void v13_block(float& acc, const float* src, const int* soff,
+                                          const float* w28, int k0, int nk, Ring3& x,
+                                          float (&wa)[28], float (&wb)[28]) {
+  // on entry: weights of source k0 in wa, rows 0 and 1 of source k0 in x.r[0], x.r[1]
+  const float* sbs[G + 1];
+#pragma unroll
+  for (int j = 0; j <= G; ++j) {
+    const int kk = k0 + j < nk ? k0 + j : nk - 1;
+    sbs[j] = src + soff[kk];
+  }
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    // next source's weights into the other buffer
+    {
+      const int kn = k0 + j + 1 < nk ? k0 + j + 1 : nk - 1;
+      float* wd = (j & 1) ? wa : wb;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        const float4 v = reinterpret_cast<const float4*>(w28 + kn * 28)[q];
+        wd[4 * q] = v.x; wd[4 * q + 1] = v.y; wd[4 * q + 2] = v.z; wd[4 * q + 3] = v.w;
+      }
+    }
+    const float* wcur = (j & 1) ? wb : wa;
+#pragma unroll
+    for (int v = 0; v < KY; ++v) {
+      const int row = j * KY + v;
+      // prefetch row + 2 (this source's row v+2, or the next source's)
+      const float* nrow = v + 2 < KY ? sbs[j] + (v + 2) * SW : sbs[j + 1] + (v + 2 - KY) * SW;
+#pragma unroll
+      for (int u = 0; u < KX; ++u) x.r[(row + 2) % 3][u] = nrow[u];
+#pragma unroll
+      for (int u = 0; u < KX; ++u)
+        acc = __fadd_rn(acc, __fmul_rn(wcur[v * KX + u], x.r[row % 3][u]));
+    }
+  }
+}
+__device__ __forceinline__ float cell_v13(float acc, const float* src, const int* soff,
+                                          const float* w28) {
+  Ring3 x;
+  float wa[28], wb[28];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const float4 v = reinterpret_cast<const float4*>(w28)[q];
+    wa[4 * q] = v.x; wa[4 * q + 1] = v.y; wa[4 * q + 2] = v.z; wa[4 * q + 3] = v.w;
+  }
+  const float* sb = src + soff[0];
+#pragma unroll
+  for (int u = 0; u < KX; ++u) { x.r[0][u] = sb[u]; x.r[1][u] = sb[SW + u]; }
+  int k = 0;
+  for (; k + 6 <= NK; k += 6) v13_block<6>(acc, src, soff, w28, k, NK, x, wa, wb);
+  // tail: the ring offsets restart at 0 because 6*KY rows is a multiple of 3
+  for (; k < NK; ++k) {
+    // one source at a time: row buffers rotate by KY per source -> use block<1>
+    // only when KY % 3 == 0; otherwise re-seed the ring (rare: < 6 sources)
+    const float* s0 = src + soff[k];
+#pragma unroll
+    for (int u = 0; u < KX; ++u) { x.r[0][u] = s0[u]; x.r[1][u] = s0[SW + u]; }
+    float* wsrc = (k & 1) ? wb : wa;
+    (void)wsrc;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(w28 + k * 28)[q];
+      wa[4 * q] = v.x; wa[4 * q + 1] = v.y; wa[4 * q + 2] = v.z; wa[4 * q + 3] = v.w;
+    }
+    v13_block<1>(acc, src, soff, w28, k, NK, x, wa, wb);
+  }
+  return acc;
+}
+
 template <int V>
 __global__ void bench(const float* gsrc, const float* gw, float* out, long long* cyc, int items) {
   __shared__ float src[NK * SHW];
@@ -217,7 +445,7 @@ __global__ void bench(const float* gsrc, const float* gw, float* out, long long*
   __shared__ int soff[NK];
   for (int i = threadIdx.x; i < NK * SHW; i += blockDim.x) src[i] = gsrc[i];
   for (int i = threadIdx.x; i < NK * 28; i += blockDim.x)
-    w[i] = V == 2 ? ((i % 28) < KK ? gw[(i / 28) * KK + i % 28] : 0.f) : (i < NK * KK ? gw[i] : 0.f);
+    w[i] = (V == 2 || V == 7 || V >= 12) ? ((i % 28) < KK ? gw[(i / 28) * KK + i % 28] : 0.f) : (i < NK * KK ? gw[i] : 0.f);
   for (int i = threadIdx.x; i < NK; i += blockDim.x) soff[i] = i * SHW;
   __syncthreads();
   const int it = threadIdx.x;
@@ -230,6 +458,13 @@ __global__ void bench(const float* gsrc, const float* gw, float* out, long long*
   else if (V == 1) a = cell_v1(0.1f, base, soff, w);
   else if (V == 2) a = cell_v2(0.1f, base, soff, w);
   else if (V == 3) a = cell_v3(0.1f, base, soff, w);
+  else if (V == 7) a = cell_v7(0.1f, base, soff, w);
+  else if (V == 8) a = cell_v8(0.1f, base, soff, w);
+  else if (V == 9) a = cell_v9(0.1f, base, soff, w);
+  else if (V == 10) a = cell_v10(0.1f, base, soff, w);
+  else if (V == 11) a = cell_v11(0.1f, base, soff, w);
+  else if (V == 12) a = cell_v12(0.1f, base, soff, w);
+  else if (V == 13) a = cell_v13(0.1f, base, soff, w);
   else if (V >= 5) {
     const int n = V == 5 ? 4 : 2;
     const int rr = (it / 2) % 9, cc = n * (it % 2);
@@ -277,8 +512,8 @@ int main() {
   for (int i = 0; i < NK * KK; ++i) hw[i] = rnd() * 0.1f - 0.05f;
   cudaMemcpy(gs, hs, sizeof(hs), cudaMemcpyHostToDevice);
   cudaMemcpy(gw, hw, sizeof(hw), cudaMemcpyHostToDevice);
-  for (int items : {32, 64, 128}) {
-    for (int v = 0; v < 7; ++v) {
+  for (int items : {32, 96}) {
+    for (int v = 7; v < 14; ++v) {
       for (int rep = 0; rep < 2; ++rep) {
         if (v == 0) bench<0><<<1, 128>>>(gs, gw, out, cyc, items);
         if (v == 1) bench<1><<<1, 128>>>(gs, gw, out, cyc, items);
@@ -287,6 +522,13 @@ int main() {
         if (v == 4) bench<4><<<1, 128>>>(gs, gw, out, cyc, items);
         if (v == 5) bench<5><<<1, 128>>>(gs, gw, out, cyc, items);
         if (v == 6) bench<6><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 7) bench<7><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 8) bench<8><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 9) bench<9><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 10) bench<10><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 11) bench<11><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 12) bench<12><<<1, 128>>>(gs, gw, out, cyc, items);
+        if (v == 13) bench<13><<<1, 128>>>(gs, gw, out, cyc, items);
       }
       cudaDeviceSynchronize();
       long long hc[128];
