@@ -495,7 +495,8 @@ def measure_config(ctx, name, steps, warmup, sm_mhz, full):
     step_ms, total = ctx.timed(
         lambda k: training.train_sequence_async(net, dd, orders[k % 4], ETA, ctx.sh),
         steps, warmup)
-    launches = _lib.kernel_launches() - launches0 - warmup
+    # the counter also saw the warm-up steps: scale to the timed ones
+    launches = (_lib.kernel_launches() - launches0) * steps // (steps + warmup)
     value = ctx.world * n_img * steps / (total / 1e3)
     block = {"value": value, "unit": UNIT, "ms_per_step": total / steps,
              "imgs_per_step": n_img, "train_mflop_per_img": work["train"] / 1e6,

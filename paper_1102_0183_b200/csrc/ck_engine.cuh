@@ -110,8 +110,18 @@ struct Program {
   Op ops[kMaxOps];
 };
 
+// Phase 0 of a program that only loads the input and runs the image-
+// processing layer: skipped (barrier included) when the job carries that
+// layer precomputed (Job::pre).
+__host__ __device__ constexpr bool phase0_input_only(const struct Program& P);
+
 enum ProgId { PROG_TRAIN = 0, PROG_FORWARD = 1, PROG_BACKWARD = 2, PROG_APPLY = 3,
               PROG_EVAL = 4, N_PROGS = 5 };
+
+__host__ __device__ constexpr bool phase0_input_only(const Program& P) {
+  return P.n_phases > 1 && P.begin[1] - P.begin[0] == 2 &&
+         P.ops[P.begin[0]].kind == OP_LOAD_INPUT && P.ops[P.begin[0] + 1].kind == OP_IMGPROC;
+}
 
 // A net's geometry and phase programs: plain values (compile-time constants
 // in the specialised kernels, a shared-memory copy in the generic ones).
@@ -190,6 +200,9 @@ struct Job {
   int sub_rank;
   int full;                // 1: also compute values nothing downstream reads (conv
                            // cells a pool truncates, dense conv deltas) for readback
+  const float* pre;        // training: the image-processing layer of visit t at
+                           // pre + t * L[1].cells, computed by a batched prepass
+                           // (ck_net.cu contrast_pre_kernel); null: phase 0 runs
 };
 
 struct Ctx {
@@ -214,7 +227,15 @@ struct TeamCtx {
   const uint8_t* in_u8;
   const float* in_lut;
   const float* in_f32;
+  const float* pre;        // this image's precomputed image-processing layer (or null)
 };
+
+// The y of layer S as the ops below read it: the precomputed image-processing
+// layer of the current image when the job carries one, else the act arena.
+__device__ __forceinline__ const float* layer_y(const LayerDev& S, const float* act,
+                                                const TeamCtx& tm) {
+  return (S.kind == L_IMGPROC && tm.pre) ? tm.pre : act + S.y_off;
+}
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
@@ -368,6 +389,35 @@ __device__ __forceinline__ void op_load_input(const NetGeo& N, const NetPtr& R, 
   }
 }
 
+// One contrast response cell q (>= C*h*w) of layer L over the image `src`
+// (C dense channels) and the filters `kbase`: kImgLanes lanes per cell, lane
+// `sub` takes the filter rows i = sub, sub + kImgLanes, ... (f64 fma chains),
+// combined by a fixed xor tree -- the same bits wherever it runs (the
+// per-image op below and the batched prepass, ck_net.cu).  The f64 result
+// rounds to the same f32 as the reference's f64 sum (any f64
+// order gave 0 mismatches).
+__device__ __forceinline__ double contrast_cell(const LayerDev& L, const float* src,
+                                                const double* kbase, int q, int sub,
+                                                unsigned gmask) {
+  const int hw = L.h * L.w, C = L.src_maps;
+  const int cy = L.fh / 2, cx = L.fw / 2, taps = L.fh * L.fw;
+  const int o = q / hw, pix = q % hw;
+  const int y = pix / L.w, x = pix % L.w;
+  const int f = (o - C) / C, c = (o - C) % C;
+  const float* s = src + c * hw;
+  const double* k = kbase + (int64_t)f * taps;
+  double acc = 0.0;
+  for (int i = sub; i < L.fh; i += kImgLanes) {
+    const float* srow = s + min(max(y + i - cy, 0), L.h - 1) * L.w;
+    const double* krow = k + i * L.fw;
+    for (int j = 0; j < L.fw; ++j)
+      acc = fma(krow[j], (double)srow[min(max(x + j - cx, 0), L.w - 1)], acc);
+  }
+#pragma unroll
+  for (int m = kImgLanes / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(gmask, acc, m);
+  return acc;
+}
+
 // correlate(mode="nearest") per (filter, channel): f64 sum, one rounding.
 __device__ __forceinline__ void op_imgproc(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                            const TeamCtx& tm) {
@@ -415,20 +465,7 @@ __device__ __forceinline__ void op_imgproc(const NetGeo& N, const NetPtr& R, con
   const unsigned gmask = ((1u << kImgLanes) - 1) << (lane & ~(kImgLanes - 1));
   for (int r = rs.b + threadIdx.x / kImgLanes; r < rs.e; r += blockDim.x / kImgLanes) {
     const int q = C * hw + r;
-    const int o = q / hw, pix = q % hw;
-    const int y = pix / L.w, x = pix % L.w;
-    const int f = (o - C) / C, c = (o - C) % C;
-    const float* s = src + c * hw;
-    const double* k = kbase + (int64_t)f * taps;
-    double acc = 0.0;
-    for (int i = sub; i < L.fh; i += kImgLanes) {
-      const float* srow = s + min(max(y + i - cy, 0), L.h - 1) * L.w;
-      const double* krow = k + i * L.fw;
-      for (int j = 0; j < L.fw; ++j)
-        acc = fma(krow[j], (double)srow[min(max(x + j - cx, 0), L.w - 1)], acc);
-    }
-#pragma unroll
-    for (int m = kImgLanes / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(gmask, acc, m);
+    const double acc = contrast_cell(L, src, kbase, q, sub, gmask);
     if (sub == 0) out[q] = (float)acc;
   }
 }
@@ -657,7 +694,7 @@ __device__ __forceinline__ void conv_fwd_chunk(const NetGeo& N, const NetPtr& R,
   float* ss = ws + n_w;
   const bool w_in_smem = (k1 - k0) + n_w <= tm.smem_floats;
   const bool s_in_smem = w_in_smem && (k1 - k0) + n_w + n_src <= tm.smem_floats;
-  const float* src_g = act + S.y_off;
+  const float* src_g = layer_y(S, act, tm);
   for (int k = threadIdx.x; k < k1 - k0; k += blockDim.x) soff[k] = t_fwd_src(R, L, (k0 + k)) * (S.h * S.w);
   if (w_in_smem)
     for (int i = threadIdx.x; i < n_w; i += blockDim.x) cp_async4(ws + i, arena + w0 + i);
@@ -716,7 +753,7 @@ __device__ __forceinline__ void store_pooled(const LayerDev& P, float* act, int 
 __device__ __forceinline__ void op_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                             const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
-  const float* src = act + S.y_off;
+  const float* src = layer_y(S, act, tm);
   float* y = act + L.y_off;
   int* arg = reinterpret_cast<int*>(act + L.arg_off);
   const int hw = L.h * L.w;
@@ -787,7 +824,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
   CK_SUBT(tm, 1);
   const Span sp = cta_span(P.cells, tm);
   int used = 0;
-  const float* src_g = act + S.y_off;
+  const float* src_g = layer_y(S, act, tm);
   const float* src = src_g;
   int sw = S.w;               // row pitch of `src` (L.spitch when staged pitched)
   if (li == 1) {
@@ -1052,7 +1089,7 @@ __device__ __forceinline__ void op_fc_fwd(const NetGeo& N, const NetPtr& R, cons
   const int n_tiles = (n_out + kFcTile - 1) / kFcTile;
   if (tm.rank >= n_tiles) return;
   int used = 0;
-  const float* x = stage(act + S.y_off, n_in, tm, used);
+  const float* x = stage(layer_y(S, act, tm), n_in, tm, used);
   double* red = reinterpret_cast<double*>(tm.smem + used);   // [kFcSlices][kFcTile]
   used += 2 * kFcSlices * kFcTile;
   float* out_a = tm.smem + used;
@@ -1152,7 +1189,7 @@ __device__ __forceinline__ void fc_bwd_rows(const NetGeo& N, const NetPtr& R, co
 __device__ __forceinline__ void op_fc_bwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags,
                                           float eta_f, float* act, const TeamCtx& tm) {
   const int li = &L - N.L;
-  fc_bwd_rows(N, R, L, li, flags, eta_f, act, act + N.L[li - 1].y_off, act + L.d_off, tm);
+  fc_bwd_rows(N, R, L, li, flags, eta_f, act, layer_y(N.L[li - 1], act, tm), act + L.d_off, tm);
 }
 
 // The output layer in one phase: every CTA recomputes the output layer's
@@ -1166,7 +1203,7 @@ __device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, cons
   const LayerDev& S = N.L[li - 1];
   float* act = ctx.act;
   int used = 0;
-  const float* x = stage(act + S.y_off, S.cells, tm, used);
+  const float* x = stage(layer_y(S, act, tm), S.cells, tm, used);
   const float* W = stage(R.params + L.p_off, S.cells * L.cells, tm, used, 1 << 14);
   // fused: H's pre-activations too (its f'(a) below), in the same round trip
   const float* ha = (flags & F_FUSE_BELOW) ? stage(act + S.a_off, S.cells, tm, used) : nullptr;
@@ -1235,7 +1272,7 @@ __device__ __forceinline__ void op_fc_out(const NetGeo& N, const NetPtr& R, cons
       gW[i * L.cells + j] = __fmul_rn(x[i], dl[j]);
     }
   }
-  fc_bwd_rows(N, R, H, li - 1, flags & F_UPDATE, job.eta_f, act, act + N.L[li - 2].y_off, dh, tm);
+  fc_bwd_rows(N, R, H, li - 1, flags & F_UPDATE, job.eta_f, act, layer_y(N.L[li - 2], act, tm), dh, tm);
   __syncthreads();
 }
 
@@ -1495,7 +1532,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
   const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int* wrc_g = reinterpret_cast<const int*>(act + P.wrc_off);
   const float* wd_g = act + P.wd_off;
-  const float* ys_g = act + S.y_off;
+  const float* ys_g = layer_y(S, act, tm);
   const int cap = tm.smem_floats - 16;
   const int split = L.wg_split;
   CK_SUBT(tm, 10);
@@ -1713,7 +1750,7 @@ __device__ __forceinline__ void op_conv_bwd(const NetGeo& N, const NetPtr& R, co
   const int lane = lane_id();
   int used = 0;
   const float* dl = stage(act + L.d_off, L.cells, tm, used);
-  const float* ys = stage(act + S.y_off, S.cells, tm, used);
+  const float* ys = stage(layer_y(S, act, tm), S.cells, tm, used);
   stage_sync();
   const int n_w = L.n_pairs;
   const int total = n_w + L.maps;

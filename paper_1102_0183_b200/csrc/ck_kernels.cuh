@@ -171,6 +171,8 @@ __device__ __forceinline__ void team_loop(const NetGeo& N, const NetPtr& R, cons
     ctx.img = job.order ? (int64_t)__ldg(job.order + t) : job.first + t;
     ctx.label = job.labels ? __ldg(job.labels + ctx.img) : -1;
     set_input(N, job, ctx, tm);
+    tm.pre = (job.pre && N.L[1].kind == L_IMGPROC) ? job.pre + ctx.t * (int64_t)N.L[1].cells
+                                                   : nullptr;
     long long* prof = (job.prof && team == 0 && t < job.prof_images)
                           ? job.prof + t * prof_stride : nullptr;
     if (prof && rank == 0 && threadIdx.x == 0) prof[0] = globaltimer();
@@ -203,7 +205,8 @@ struct InterpPhases {
   __device__ __forceinline__ void operator()(const Job& job, Ctx& ctx, TeamCtx& tm,
                                              double* scratch, After& after) const {
     const Program& P = N.prog[job.prog];
-    for (int ph = 0; ph < P.n_phases; ++ph) {
+    const int ph0 = (tm.pre && phase0_input_only(P)) ? 1 : 0;   // precomputed input layers
+    for (int ph = ph0; ph < P.n_phases; ++ph) {
       tm.ph = ph;
       CK_SUBT(tm, 0);
       run_phase(N, R, P, ph, job, ctx, tm, scratch);
@@ -253,6 +256,12 @@ struct SpecPhase {
   template <class After>
   __device__ static __forceinline__ void run(const NetPtr& R, const Job& job, Ctx& ctx,
                                              TeamCtx& tm, double* scratch, After& after) {
+    if constexpr (PH == 0 && phase0_input_only(Spec::geo().prog[PROG])) {
+      if (tm.pre) {           // input layers precomputed by the batched prepass
+        SpecPhase<Spec, PROG, 1>::run(R, job, ctx, tm, scratch, after);
+        return;
+      }
+    }
     if constexpr (PH < Spec::geo().prog[PROG].n_phases) {
       tm.ph = PH;
       CK_SUBT(tm, 0);
@@ -327,6 +336,7 @@ __device__ __forceinline__ void eval_loop(const NetGeo& N, const Job& job, unsig
   tm.gwarps = blockDim.x >> 5;
   tm.smem = reinterpret_cast<float*>(work);
   tm.smem_floats = job.eval_floats;
+  tm.pre = nullptr;
   Ctx ctx;
   ctx.act = job.eval_scratch + (int64_t)blockIdx.x * N.act_size;
   const LayerDev& O = N.L[N.n_layers - 1];

@@ -52,6 +52,8 @@ struct ck_net {
   double* d_targets = nullptr;    // single-step staging
   double* d_loss = nullptr;       // per-launch loss total (1 double)
   float* d_eval = nullptr;        // eval scratch arenas
+  float* d_pre = nullptr;         // training: precomputed image-processing layers
+  int64_t pre_cap = 0;            // floats
   int eval_ctas = 0;
   int64_t n_params = 0;
   int team_kind = CK_TEAM_AUTO;   // resolved per launch (resolve_team)
@@ -789,6 +791,76 @@ std::string spec_source(const NetGeo& g, const char* name) {
   return o;
 }
 
+// Batched image-processing prepass for training launches: the contrast layer
+// depends on the input image only, so instead of a team phase per image (all
+// CTAs, then a barrier) every visited image's layer is computed up front by
+// this kernel -- kPreSplit CTAs per image, the image staged in shared memory,
+// contrast_cell's arithmetic (the per-image op's bits exactly).  Output: the
+// layer's y (original channels, then the responses) of visit t at out + t *
+// L.cells; the training kernel reads it (Job::pre) and skips phase 0.
+constexpr int kPreSplit = 4;
+__global__ void __launch_bounds__(256)
+contrast_pre_kernel(LayerDev L, const double* __restrict__ filt, const uint8_t* images,
+                    const float* lut, const int32_t* order, int64_t n, int in_cells,
+                    float* out) {
+  extern __shared__ float img[];
+  const int64_t t = blockIdx.x / kPreSplit;
+  const int part = blockIdx.x % kPreSplit;
+  if (t >= n) return;
+  const int64_t im = order ? (int64_t)__ldg(order + t) : t;
+  if (lut)
+    for (int i = threadIdx.x; i < in_cells; i += blockDim.x)
+      img[i] = __ldg(lut + __ldg(images + im * in_cells + i));
+  else
+    for (int i = threadIdx.x; i < in_cells; i += blockDim.x)
+      img[i] = __ldg(reinterpret_cast<const float*>(images) + im * in_cells + i);
+  __syncthreads();
+  float* o = out + t * (int64_t)L.cells;
+  const int hw = L.h * L.w, C = L.src_maps, n_resp = L.cells - C * hw;
+  if (part == 0)
+    for (int i = threadIdx.x; i < C * hw; i += blockDim.x) o[i] = img[i];
+  const int lane = threadIdx.x & 31, sub = threadIdx.x % kImgLanes;
+  const unsigned gmask = ((1u << kImgLanes) - 1) << (lane & ~(kImgLanes - 1));
+  const int chunk = (n_resp + kPreSplit - 1) / kPreSplit;
+  const int r1 = min(n_resp, (part + 1) * chunk);
+  for (int r = part * chunk + threadIdx.x / kImgLanes; r < r1; r += blockDim.x / kImgLanes) {
+    const double acc = contrast_cell(L, img, filt + L.o_filt, C * hw + r, sub, gmask);
+    if (sub == 0) o[C * hw + r] = (float)acc;
+  }
+}
+
+// The prepass for a training launch over `n` visits (nullptr in *pre when the
+// net has no image-processing layer, or CKB200_NO_PRE is set: A/B switch).
+int run_prepass(ck_net* net, const uint8_t* images, const float* lut, const int32_t* order,
+                int64_t n, cudaStream_t st, const float** pre) {
+  *pre = nullptr;
+  const NetGeo& N = net->h;
+  if (N.n_layers < 2 || N.L[1].kind != L_IMGPROC || getenv("CKB200_NO_PRE")) return CK_OK;
+  const int64_t need = n * (int64_t)N.L[1].cells;
+  if (need > net->pre_cap) {
+    CK_CUDA_TRY(cudaStreamSynchronize(st));
+    cudaFree(net->d_pre);
+    net->d_pre = nullptr;
+    net->pre_cap = 0;
+    CK_CUDA_TRY(cudaMalloc((void**)&net->d_pre, sizeof(float) * need));
+    net->pre_cap = need;
+  }
+  const size_t smem = sizeof(float) * N.in_cells;
+  static bool attr = false;
+  if (!attr) {
+    CK_CUDA_TRY(cudaFuncSetAttribute(contrast_pre_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  CK_CHECK(smem <= 200 * 1024, CK_E_DIMENSION, "input image too large for the prepass");
+  contrast_pre_kernel<<<(unsigned)(n * kPreSplit), 256, smem, st>>>(
+      N.L[1], net->d_filters, images, lut, order, n, N.in_cells, net->d_pre);
+  count_launch();
+  CK_CUDA_TRY(cudaGetLastError());
+  *pre = net->d_pre;
+  return CK_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -873,6 +945,7 @@ int ck_net_destroy(ck_net* net) {
   cudaFree(net->d_targets);
   cudaFree(net->d_loss);
   cudaFree(net->d_eval);
+  cudaFree(net->d_pre);
   delete net;
   return CK_OK;
 }
@@ -1101,7 +1174,9 @@ int ck_net_train_epoch(ck_net* net, const uint8_t* images, const float* lut,
   job.eta_f = (float)eta;
   job.losses = losses;
   job.loss_total = net->d_loss;
-  int rc = launch_teams(&net, 1, job, (cudaStream_t)stream);
+  int rc = run_prepass(net, images, lut, order, n, (cudaStream_t)stream, &job.pre);
+  if (rc) return rc;
+  rc = launch_teams(&net, 1, job, (cudaStream_t)stream);
   if (rc) return rc;
   if (mean_loss) {
     double tot = 0;
@@ -1126,6 +1201,7 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
   const int64_t stride = 1 + (int64_t)np * (1 + ctas);
   long long* d_prof = nullptr;
   CK_CUDA_TRY(cudaMalloc((void**)&d_prof, sizeof(long long) * n * stride));
+  CK_CUDA_TRY(cudaMemset(d_prof, 0, sizeof(long long) * n * stride));
   Job job = empty_job(PROG_TRAIN);
   job.images = images;
   job.lut = lut;
@@ -1136,7 +1212,8 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
   job.loss_total = net->d_loss;
   job.prof = d_prof;
   job.prof_images = n;
-  int rc = launch_teams(&net, 1, job, net->stream);
+  int rc = run_prepass(net, images, lut, order, n, net->stream, &job.pre);
+  if (rc == CK_OK) rc = launch_teams(&net, 1, job, net->stream);
   std::vector<long long> h((size_t)(n * stride));
   if (rc == CK_OK) {
     cudaError_t e = cudaMemcpyAsync(h.data(), d_prof, sizeof(long long) * h.size(),
@@ -1148,12 +1225,20 @@ int ck_net_profile_epoch(ck_net* net, const uint8_t* images, const float* lut,
   if (rc) return rc;
   // phase_ns[p]: slowest CTA's work (phase start -> its work end);
   // phase_ns[np + p]: barrier latency (slowest work end -> barrier exit)
+  // (a phase skipped because its layers were precomputed -- Job::pre -- has
+  // no records: it reads as zero work and the next phase starts at r[0])
   for (int p = 0; p < np; ++p) {
     long long work = 0, bar = 0;
     for (int64_t t = 0; t < n; ++t) {
       const long long* r = h.data() + t * stride;
-      const long long start = p == 0 ? r[0] : r[1 + (p - 1) * (1 + ctas)];
       const long long* ph = r + 1 + p * (1 + ctas);
+      if (ph[0] == 0) continue;
+      long long start = r[0];
+      for (int q = p - 1; q >= 0; --q)
+        if (r[1 + q * (1 + ctas)] != 0) {
+          start = r[1 + q * (1 + ctas)];
+          break;
+        }
       long long wmax = start;
       for (int c = 0; c < ctas; ++c) wmax = std::max(wmax, ph[1 + c]);
       work += wmax - start;

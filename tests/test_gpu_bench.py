@@ -40,7 +40,7 @@ def test_bench_line_contract():
                   "--imgs-per-step", "64", "--cpu-seconds", "0.3", "--cpu-windows", "1")
     for k in REQUIRED:
         assert k in d, k
-    assert d["value"] > 0 and d["gpu_launches"] == 3
+    assert d["value"] > 0 and d["gpu_launches"] == 3     # C1: one launch per step
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["value"] > 0
     assert 0 < d["roofline"]["frac"] < 1
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1

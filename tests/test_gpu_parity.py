@@ -434,3 +434,27 @@ def test_specialised_kernels_bit_identical_to_generic(name):
     np.testing.assert_array_equal(o_fast, o_slow)
     fast.close()
     slow.close()
+
+
+def test_contrast_prepass_bit_identical():
+    """Training launches of nets with an image-processing layer compute it for
+    every visited image in a batched prepass (ck_net.cu contrast_pre_kernel)
+    and skip the per-image phase 0; the result must equal the per-image path
+    bit for bit (CKB200_NO_PRE=1 disables the prepass)."""
+    import os
+    from paper_1102_0183_b200.configs import spec_for
+    spec = spec_for("C3")
+    data = ck.make_glyph_dataset(6, spec.n_classes, 48, seed=8, channels=2)
+    cfg = ck.TrainConfig(epochs=1, eta0=1e-3, seed=2)
+    a = ck.NetworkState(spec, 3)
+    b = ck.NetworkState(spec, 3)
+    os.environ["CKB200_NO_PRE"] = "1"
+    try:
+        m_b = ck.train_epoch(b, data, cfg, 0)
+    finally:
+        del os.environ["CKB200_NO_PRE"]
+    m_a = ck.train_epoch(a, data, cfg, 0)
+    assert m_a == m_b
+    np.testing.assert_array_equal(a.flat_parameters(), b.flat_parameters())
+    a.close()
+    b.close()
