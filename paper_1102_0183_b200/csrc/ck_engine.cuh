@@ -806,6 +806,102 @@ __device__ __forceinline__ float conv_value_global(const NetPtr& R, const LayerD
   return acc;
 }
 
+// conv + pool for a FULL connection table whose source layer does not fit the
+// scratch (C4'): one cell per thread on the reference-order chain, the
+// source maps staged in passes of as many whole maps as fit (the pool's
+// pre-pitched copy when it has one), every chain continuing where the last
+// pass left it -- the order stays bias, then k = 0, 1, ... .  Returns false
+// (nothing done) when the CTA's cells exceed one per thread.
+template <int KX, int KY>
+__device__ __forceinline__ bool conv_pool_fwd_passes(const NetGeo& N, const NetPtr& R,
+                                                     const LayerDev& L, int flags, bool full,
+                                                     float* act, const TeamCtx& tm) {
+  constexpr int KK = KX * KY, KKP = (KK + 3) & ~3;
+  const int li = &L - N.L;
+  const LayerDev& S = N.L[li - 1];
+  const LayerDev& P = N.L[li + 1];
+  const int hw = L.h * L.w, phw = P.h * P.w, blk = P.px * P.py;
+  const Span sp = cta_span(P.cells, tm);
+  const int n_items = (sp.e - sp.b) * blk;
+  if (n_items > (int)blockDim.x) return false;     // uniform per CTA
+  if (sp.b >= sp.e) return true;
+  const float* arena = R.params + L.p_off;
+  const int d0 = sp.b / phw, d1 = (sp.e - 1) / phw, nd = d1 - d0 + 1;
+  const int SM = S.maps;
+  const bool pitched = S.ypitch > 0;
+  const int sw = pitched ? S.ypitch : S.w, smap = S.h * sw;
+  const float* src = pitched ? act + S.yp_off : layer_y(S, act, tm);
+  // scratch: [weights nd*SM*KKP | biases nd | map offsets | pre-activations | source pass]
+  float* ws = tm.smem;
+  float* bs = ws + nd * SM * KKP;
+  int* soff = reinterpret_cast<int*>(bs + ((nd + 3) & ~3));
+  float* ybuf = reinterpret_cast<float*>(soff) + ((SM + 3) & ~3);
+  float* sp_buf = ybuf + ((n_items + 3) & ~3);
+  const int room = tm.smem_floats - (int)(sp_buf - tm.smem);
+  const int per_pass = min(SM, room / smap);
+  if (per_pass < 1) return false;
+  for (int e = threadIdx.x; e < nd * SM * KK; e += blockDim.x) {
+    const int j = e / KK, t = e - j * KK;        // pair (d0 + j / SM, j % SM)
+    const int d = d0 + j / SM;
+    cp_async4(ws + j * KKP + t, arena + ((int64_t)d * SM + j % SM) * KK + d + t + (int64_t)0);
+  }
+  for (int d = d0 + threadIdx.x; d <= d1; d += blockDim.x)
+    cp_async4(bs + (d - d0), arena + (int64_t)(d + 1) * SM * KK + d);
+  for (int k = threadIdx.x; k < SM; k += blockDim.x) soff[k] = k * smap;
+  const int it = threadIdx.x;
+  const bool mine = it < n_items;
+  const int qq = sp.b + it / blk, t = it % blk;
+  const int d = qq / phw, pp = qq % phw;
+  const int r = (pp / P.w) * P.py + t / P.px, c = (pp % P.w) * P.px + t % P.px;
+  float acc = 0.0f;
+  for (int m0 = 0; m0 < SM; m0 += per_pass) {
+    const int m1 = min(SM, m0 + per_pass);
+    if (m0 > 0) __syncthreads();                 // the previous pass is consumed
+    int u = (int)(sp_buf - tm.smem);
+    stage(src + (int64_t)m0 * smap, (m1 - m0) * smap, tm, u);
+    stage_sync();
+    if (mine) {
+      if (m0 == 0) acc = bs[d - d0];
+      acc = conv_cell_smem4<KX, KY>(acc, sp_buf + (r * L.ty) * sw + c * L.tx, soff,
+                                    ws + ((d - d0) * SM + m0) * KKP, m1 - m0, sw);
+    }
+  }
+  // epilogue: a / y of the cell, then the pool of each block (strict '>')
+  const bool zero = full && (flags & F_ZERO_SELF);
+  const bool pooled_only = (flags & F_POOLED_ONLY) && !full;
+  if (mine) {
+    if (pooled_only) {
+      ybuf[it] = acc;
+    } else {
+      const int cell = d * hw + r * L.w + c;
+      const float yv = conv_act(acc);
+      act[L.a_off + cell] = acc;
+      act[L.y_off + cell] = yv;
+      ybuf[it] = yv;
+      if (zero) act[L.d_off + cell] = 0.0f;
+    }
+  }
+  __syncthreads();
+  int* parg = reinterpret_cast<int*>(act + P.arg_off);
+  int* pwrc = reinterpret_cast<int*>(act + P.wrc_off);
+  for (int qi = threadIdx.x; qi < sp.e - sp.b; qi += blockDim.x) {
+    const float* yb = ybuf + qi * blk;
+    int bt = 0;
+    float best = yb[0];
+    for (int tt = 1; tt < blk; ++tt)
+      if (yb[tt] > best) { best = yb[tt]; bt = tt; }
+    if (pooled_only) best = conv_act(best);
+    const int q2 = sp.b + qi;
+    const int d2 = q2 / phw, p2 = q2 % phw;
+    const int r2 = (p2 / P.w) * P.py + bt / P.px, c2 = (p2 % P.w) * P.px + bt % P.px;
+    store_pooled(P, act, q2, best);
+    parg[q2] = d2 * hw + r2 * L.w + c2;
+    pwrc[q2] = (r2 << 16) | c2;
+  }
+  __syncthreads();
+  return true;
+}
+
 template <int KX, int KY>
 __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, const LayerDev& L, int flags, bool full,
                               float* act, const TeamCtx& tm) {
@@ -823,6 +919,13 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
   int* pwrc = reinterpret_cast<int*>(act + P.wrc_off);
   CK_SUBT(tm, 1);
   const Span sp = cta_span(P.cells, tm);
+  if constexpr (KX > 0) {
+    // full table, source layer too big to stage whole: source passes
+    if (L.full && li > 1 && S.cells > tm.smem_floats / 2 && !full &&
+        conv_pool_fwd_passes<KX, KY>(N, R, L, flags, full, act, tm)) {
+      return;
+    }
+  }
   int used = 0;
   const float* src_g = layer_y(S, act, tm);
   const float* src = src_g;

@@ -458,3 +458,25 @@ def test_contrast_prepass_bit_identical():
     np.testing.assert_array_equal(a.flat_parameters(), b.flat_parameters())
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("name", ["C3", "C4F"])
+def test_epoch_launch_equals_single_steps(name):
+    """The epoch launch takes the throughput paths (the contrast prepass, the
+    source-pass conv of full tables too big to stage, pooled-only work); the
+    per-sample train_step takes the readback paths.  Same arithmetic: the
+    weights after the same visits are bit-identical."""
+    from paper_1102_0183_b200.configs import spec_for
+    spec = spec_for(name)
+    first = spec.layers[0]
+    data = ck.make_glyph_dataset(3, spec.n_classes, first.out_width, seed=9,
+                                 channels=first.out_maps)
+    cfg = ck.TrainConfig(epochs=1, eta0=1e-3, shuffle=False)
+    a = ck.NetworkState(spec, 4)
+    b = ck.NetworkState(spec, 4)
+    ck.train_epoch(a, data, cfg, 0)
+    for i in range(len(data)):
+        b.train_step(data.images[i], ck.targets_for(int(data.labels[i]), spec.n_classes), 1e-3)
+    np.testing.assert_array_equal(a.flat_parameters(), b.flat_parameters())
+    a.close()
+    b.close()
