@@ -18,8 +18,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.join(ROOT, "paper_1102_0183_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libckb200.so")
-SOURCES = ["ck_seam.cu", "ck_net.cu", "ck_deform.cu", "ck_tc.cu"]
-HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_kernels.cuh", "ck_host.h", "ck_specs.inc"]
+SOURCES = ["ck_seam.cu", "ck_net.cu", "ck_deform.cu", "ck_tc.cu", "ck_tct.cu"]
+HEADERS = ["ck_numerics.cuh", "ck_engine.cuh", "ck_kernels.cuh", "ck_host.h", "ck_specs.inc",
+           "ck_tc_common.cuh"]
 
 COMPILE_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -30,7 +31,8 @@ COMPILE_FLAGS = [
 LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared"]
 # per-unit extras: the tensor-core GEMMs run at register caps set by their
 # launch bounds (3-4 CTAs per SM); a spill there must fail the build
-UNIT_FLAGS = {"ck_tc.cu": ["-Xptxas=-warn-spills,-Werror"]}
+UNIT_FLAGS = {"ck_tc.cu": ["-Xptxas=-warn-spills,-Werror"],
+              "ck_tct.cu": ["-Xptxas=-warn-spills,-Werror"]}
 
 
 def _nvcc() -> str:

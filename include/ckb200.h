@@ -325,6 +325,23 @@ int ck_tc_destroy(ck_tc_eval* plan);
 int ck_tc_set_params(ck_tc_eval* plan, const float* params, ck_stream_t stream);
 int ck_tc_eval_run(ck_tc_eval* plan, const uint8_t* images, const float* lut, int64_t first,
                    int64_t n, int32_t* pred, float* outputs, ck_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Tensor-core training variant (opt-in, its own tolerance):
+ * online training of input -> (conv, stride 1 -> maxpool)+ -> fc+ nets with
+ * every conv forward, weight gradient and delta pull as a tcgen05 implicit
+ * GEMM (fp16 hi/lo split, f32 accumulation), the reference's protocol
+ * otherwise (network.py:163-282: one update per image, training.py:126-146
+ * visit order).  `params` is the net's DEVICE parameter vector
+ * (ck_net_device_params): the plan trains it in place, so the exact path and
+ * this one share the weights.  Not bit-exact: see tests/test_gpu_tct.py. */
+typedef struct ck_tct ck_tct;
+int ck_tct_create(const ck_layer_desc* layers, int n_layers, int device, float* params,
+                  ck_tct** out);
+int ck_tct_destroy(ck_tct* plan);
+int ck_tct_train_epoch(ck_tct* plan, const uint8_t* images, const float* lut,
+                       const int32_t* labels, const int32_t* order, int64_t n, double eta,
+                       double* mean_loss, ck_stream_t stream);
 /* Device pointer of a net's parameter vector (valid until ck_net_destroy). */
 int ck_net_device_params(const ck_net* net, const float** params);
 

@@ -101,6 +101,9 @@ _SIGNATURES = {
     "ck_tc_set_params": (_i32, [_vp, _vp, _vp]),
     "ck_tc_eval_run": (_i32, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp]),
     "ck_net_device_params": (_i32, [_vp, C.POINTER(_vp)]),
+    "ck_tct_create": (_i32, [C.POINTER(LayerDesc), _i32, _i32, _vp, C.POINTER(_vp)]),
+    "ck_tct_destroy": (_i32, [_vp]),
+    "ck_tct_train_epoch": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _f64, C.POINTER(_f64), _vp]),
     "ck_deform_apply": (_i32, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _vp, _i32, _vp, _vp]),
 }
 

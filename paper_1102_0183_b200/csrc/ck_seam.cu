@@ -224,30 +224,29 @@ __global__ void seam_contrast(const float* __restrict__ src, int n_ch,
 constexpr int kSeamFcSlices = 16;
 
 // a_j = f32(sum over 16 interleaved row slices of f64 fma chains) + b_j;
-// y_j = fc_act(a_j).  One thread per column (coalesced rows of W).
-__global__ void seam_fc_fwd(const float* __restrict__ x, int n_in,
-                            const float* __restrict__ W, const float* __restrict__ b,
-                            int n_out, float* a, float* y) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_out) return;
-  double part[kSeamFcSlices];
+// y_j = fc_act(a_j).  A CTA takes 32 columns x the 16 slices (thread = slice
+// sl, column j: the chain over rows i = sl, sl + 16, ...; consecutive threads
+// read consecutive columns of a row of W), the slices combined in order.
+__global__ void __launch_bounds__(32 * kSeamFcSlices)
+seam_fc_fwd(const float* __restrict__ x, int n_in, const float* __restrict__ W,
+            const float* __restrict__ b, int n_out, float* a, float* y) {
+  __shared__ double red[kSeamFcSlices][32];
+  const int col = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + col;
+  double part = 0.0;
+  if (j < n_out)
+    for (int i = sl; i < n_in; i += kSeamFcSlices)
+      part = fma((double)__ldg(x + i), (double)__ldg(W + (int64_t)i * n_out + j), part);
+  red[sl][col] = part;
+  __syncthreads();
+  if (sl == 0 && j < n_out) {
+    double acc = 0.0;
 #pragma unroll
-  for (int s = 0; s < kSeamFcSlices; ++s) part[s] = 0.0;
-  int i = 0;
-  for (; i + kSeamFcSlices <= n_in; i += kSeamFcSlices) {
-#pragma unroll
-    for (int s = 0; s < kSeamFcSlices; ++s)
-      part[s] = fma((double)x[i + s], (double)W[(int64_t)(i + s) * n_out + j], part[s]);
+    for (int s = 0; s < kSeamFcSlices; ++s) acc += red[s][col];
+    const float aj = __fadd_rn((float)acc, b[j]);
+    if (a) a[j] = aj;
+    y[j] = fc_act(aj);
   }
-#pragma unroll
-  for (int s = 0; s < kSeamFcSlices; ++s)
-    if (i + s < n_in) part[s] = fma((double)x[i + s], (double)W[(int64_t)(i + s) * n_out + j], part[s]);
-  double acc = 0.0;
-#pragma unroll
-  for (int s = 0; s < kSeamFcSlices; ++s) acc += part[s];
-  const float aj = __fadd_rn((float)acc, b[j]);
-  if (a) a[j] = aj;
-  y[j] = fc_act(aj);
 }
 
 __device__ __forceinline__ double seam_warp_sum(double v) {
@@ -453,7 +452,7 @@ int ck_fc_fwd(const float* x, int n_in, const float* weights, const float* bias,
               float* a_out, float* y_out, ck_stream_t stream) {
   CK_CHECK(n_in >= 1 && n_out >= 1, CK_E_DIMENSION, "FC sizes must be >= 1");
   CK_CHECK(x && weights && bias && y_out, CK_E_CONFIG, "null FC buffer");
-  seam_fc_fwd<<<blocks_for(n_out, 128), 128, 0, (cudaStream_t)stream>>>(
+  seam_fc_fwd<<<(n_out + 31) / 32, 32 * kSeamFcSlices, 0, (cudaStream_t)stream>>>(
       x, n_in, weights, bias, n_out, a_out, y_out);
   return finish_launch("ck_fc_fwd");
 }

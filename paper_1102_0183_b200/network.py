@@ -218,10 +218,26 @@ class NetworkState:
             self._tc_loaded[key] = self._version
         return plan
 
+    def tct_plan(self):
+        """Tensor-core TRAINING plan (ck_tct_create) over this
+        net's device parameters: it trains them in place."""
+        plan = getattr(self, "_tct_plan", None)
+        if plan is None:
+            params = C.c_void_p()
+            _lib.call("ck_net_device_params", self.handle, C.byref(params))
+            plan = C.c_void_p()
+            _lib.call("ck_tct_create", self._descs, len(self.spec.layers), self.device,
+                      params, C.byref(plan))
+            self._tct_plan = plan
+        return plan
+
     def close(self) -> None:
         for plan in getattr(self, "_tc_plans", {}).values():
             _lib.call("ck_tc_destroy", plan)
         self._tc_plans = {}
+        if getattr(self, "_tct_plan", None) is not None:
+            _lib.call("ck_tct_destroy", self._tct_plan)
+            self._tct_plan = None
         if self._handle is not None:
             _lib.call("ck_net_destroy", self._handle)
             self._handle = None
