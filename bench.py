@@ -88,6 +88,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-committee", action="store_true")
     ap.add_argument("--no-deform", action="store_true")
     ap.add_argument("--no-tc", action="store_true")
+    ap.add_argument("--tc-train", default="C4F",
+                    help="configs also trained on the tensor-core variant (SURVEY 8(f)4)")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU/gloo rehearsal of the multi-rank control flow (tests)")
     return ap.parse_args(argv)
@@ -505,6 +507,28 @@ def measure_config(ctx, name, steps, warmup, sm_mhz, full):
                                            sm_mhz, f"persistent online-training kernel "
                                                    f"({net.kernel_info()})",
                                            _traffic(name, n_img))}
+    block["train_tc"] = None
+    if name in args.tc_train.split(",") and not args.no_tc:
+        # the opt-in tensor-core training variant (ck_tct.cu): same steps,
+        # conv forward / weight gradients / pulls as tcgen05 GEMMs
+        plan = net.tct_plan()
+        tc_ms, tc_total = ctx.timed(
+            lambda k: _lib.call("ck_tct_train_epoch", plan, dd.images_ptr, dd.lut_ptr,
+                                dd.labels.data_ptr(), orders[k % 4].data_ptr(), n_img,
+                                float(ETA), None, ctx.sh), steps, warmup)
+        tc_rate = ctx.world * n_img * steps / (tc_total / 1e3)
+        peaks = load_peaks()
+        tc_peak = peaks.get("bf16_tflops", 2250.0)
+        tc_ach = work["train"] * n_img / (statistics.mean(tc_ms) / 1e3) / 1e12
+        block["train_tc"] = {
+            "value": tc_rate, "unit": UNIT, "ms_per_step": tc_total / steps,
+            "engine": "tcgen05 implicit GEMMs (fp16 hi/lo split, f32 accumulate) for conv "
+                      "forward, weight gradients and pulls; one CUDA graph per visit",
+            "tolerance": "vs the exact engine: losses 1e-4 rel, weights 2e-4 abs after an "
+                         "online run, labels >= 99% (tests/test_gpu_tct.py)",
+            "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": tc_peak,
+                         "unit": "TFLOP/s", "frac": tc_ach / tc_peak,
+                         "work": "algorithmic training FLOPs per image"}}
     block["e2e"] = None
     if not args.no_e2e:
         host = pin_dataset(make_data(spec, n_img, 2, "train"))
