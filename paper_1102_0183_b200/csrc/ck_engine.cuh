@@ -502,12 +502,7 @@ __device__ __forceinline__ float conv_cell(float acc, const float* src, const in
   return acc;
 }
 
-// conv_cell for operands that are all in shared memory (the staged path):
-// explicit ld.shared (no generic-address loads), and the raw operands of
-// source k+1 are loaded before source k's add chain runs, so the chain --
-// bias, then k, v, u in order, every product and sum rounded separately, as
-// kernels.py:78-86 -- is not stalled on load latency.  Bit-identical to
-// conv_cell.
+// explicit ld.shared helpers (32-bit shared addresses, no generic loads)
 __device__ __forceinline__ float lds_f32(unsigned addr) {
   float v;
   asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -519,49 +514,7 @@ __device__ __forceinline__ int lds_s32(unsigned addr) {
   return v;
 }
 
-template <int KX, int KY>
-__device__ __forceinline__ float conv_cell_smem(float acc, const float* src, const int* soff,
-                                                const float* w, int nk, int sw) {
-  constexpr int KK = KX * KY;
-  const unsigned s0 = (unsigned)__cvta_generic_to_shared(src);
-  const unsigned o0 = (unsigned)__cvta_generic_to_shared(soff);
-  const unsigned w0 = (unsigned)__cvta_generic_to_shared(w);
-  float xc[KK], wc[KK];
-  {
-    const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0);
-#pragma unroll
-    for (int t = 0; t < KK; ++t) {
-      xc[t] = lds_f32(sb + 4u * ((t / KX) * sw + t % KX));
-      wc[t] = lds_f32(w0 + 4u * t);
-    }
-  }
-  for (int k = 0; k < nk; ++k) {
-    float xn[KK], wn[KK];
-    const int kn = k + 1 < nk ? k + 1 : k;
-    const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0 + 4u * kn);
-    // source k+1's loads interleaved with source k's add chain: in-order
-    // issue fills the FADD latency with the loads instead of issuing all
-    // loads first
-#pragma unroll
-    for (int t = 0; t < KK; ++t) {
-      xn[t] = lds_f32(sb + 4u * ((t / KX) * sw + t % KX));
-      wn[t] = lds_f32(w0 + 4u * (kn * KK + t));
-      acc = __fadd_rn(acc, __fmul_rn(wc[t], xc[t]));
-    }
-#pragma unroll
-    for (int t = 0; t < KK; ++t) {
-      xc[t] = xn[t];
-      wc[t] = wn[t];
-    }
-  }
-  return acc;
-}
-
-// conv_cell_smem with each pair's kx*ky weights at a 16-byte aligned stride of
-// KKP = round_up(kx*ky, 4) floats: a warp (one dest map, or two) reads them
-// as broadcast ld.shared.v4 -- 4x fewer shared-memory wavefronts for the
-// weights, which with the source loads bound the chain's step rate.  Same
-// operands, same order: bit-identical to conv_cell.
+// a 16-byte shared load (the chain's weights: one broadcast wavefront for 4)
 __device__ __forceinline__ float4 lds_v4(unsigned addr) {
   float4 v;
   asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"

@@ -589,8 +589,15 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
   for (int k = 2; k + 1 < n_layers && !getenv("CKB200_NO_PITCH"); ++k) {   // A/B switch
     LayerDev& S = N.L[k - 1];
     if (N.L[k].kind != L_CONV || N.L[k + 1].kind != L_POOL || S.kind != L_POOL) continue;
+    // only when the consumer stages the layer whole or in source passes
+    // (full tables, conv_pool_fwd_passes) -- not for per-map slots
+    const bool whole = S.cells <= kTeamStageFloats / 2;
+    bool full_table = layers[k].n_pairs == N.L[k].maps * S.maps;
+    for (int p = 0; full_table && p < layers[k].n_pairs; ++p)
+      full_table = layers[k].fwd_srcs[p] == p % S.maps;
+    if (!whole && !full_table) continue;
     const int pitch = choose_src_pitch(N.L[k], S, N.L[k + 1]);
-    if (pitch <= S.w) continue;
+    if (pitch <= S.w || (whole && S.maps * S.h * pitch > kTeamStageFloats / 8 * 5)) continue;
     N.L[k].spitch = pitch;
     S.ypitch = pitch;
     S.yp_off = a_cursor;
@@ -656,16 +663,17 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
         full = fwd_src[p] == p % n_src && pair_dst[p] == p / n_src;
       N.L[k].full = full ? 1 : 0;
     }
-    // gather pull: measured faster than the stream scatter only for very wide
+    // gather pull: measured faster than the stream scatter for very wide
     // backward lists (C4': 300 dests per source, 399 -> 156 us per image in
-    // the pull phase; C1-C4 are faster with the scatter) -- and it needs all
-    // winners + the widest source's backward kernels staged
+    // the pull phase) and for 2x2 kernels (C4 conv2: 28 -> 25 us); C1-C3
+    // (5x5) are faster with the scatter -- and it needs all winners + the
+    // widest source's backward kernels staged
     if (k + 1 < n_layers && N.L[k].pullg) {
       const int phw = N.L[k + 1].h * N.L[k + 1].w;
       const int widest = *std::max_element(count.begin(), count.end());
       const char* pm = getenv("CKB200_PULL");
       const bool forced = pm && strcmp(pm, "gather") == 0;
-      if ((widest < 128 && !forced) ||
+      if ((widest < 128 && D.kx * D.ky > 4 && !forced) ||
           2 * ((L.maps * phw + 3) & ~3) + widest * D.kx * D.ky > kTeamStageFloats)
         N.L[k].pullg = 0;
     }
