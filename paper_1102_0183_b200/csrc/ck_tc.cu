@@ -416,6 +416,53 @@ __global__ void __launch_bounds__(256) contrast_kernel(const float* __restrict__
   }
 }
 
+// The contrast responses when every filter is low-rank (hat<N> is a
+// difference of two separable Gaussians: rank 2): filter f = sum_r u_fr v_fr^T,
+// so a response is R horizontal passes (fw taps) then R vertical passes (fh
+// taps) -- 2R(fh+fw) instead of fh*fw multiply-adds per cell (hat21: 84 vs
+// 441).  One CTA per (image, channel): the replicated-border window and the
+// horizontal results of every (filter, rank term) in shared memory.  f32;
+// the factors come from an f64 eigendecomposition on the host (within this
+// path's tolerance; the exact engine keeps the reference's f64 correlation).
+__global__ void __launch_bounds__(256) contrast_sep_kernel(
+    const float* __restrict__ X, int C, int H, int W, const float* __restrict__ uv, int F, int R,
+    int fh, int fw, float* __restrict__ Y, int out_maps) {
+  extern __shared__ float sm[];
+  const int cy = fh / 2, cx = fw / 2;
+  const int PW = W + fw - 1, PHh = H + fh - 1;
+  float* win = sm;                             // PHh x PW
+  float* hor = win + PHh * PW;                 // [F*R][PHh][W]
+  float* fac = hor + (size_t)F * R * PHh * W;  // per (f, r): u (fh) then v (fw)
+  const int64_t img = blockIdx.x / C;
+  const int c = blockIdx.x % C;
+  const float* src = X + (img * C + c) * (int64_t)H * W;
+  for (int i = threadIdx.x; i < PHh * PW; i += blockDim.x) {
+    const int r = min(max(i / PW - cy, 0), H - 1), q = min(max(i % PW - cx, 0), W - 1);
+    win[i] = src[r * W + q];
+  }
+  for (int i = threadIdx.x; i < F * R * (fh + fw); i += blockDim.x) fac[i] = uv[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < F * R * PHh * W; i += blockDim.x) {
+    const int fr = i / (PHh * W), y = (i / W) % PHh, x = i % W;
+    const float* v = fac + fr * (fh + fw) + fh;
+    const float* w = win + y * PW + x;
+    float acc = 0.f;
+    for (int j = 0; j < fw; ++j) acc = fmaf(v[j], w[j], acc);
+    hor[i] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < F * H * W; i += blockDim.x) {
+    const int f = i / (H * W), y = (i / W) % H, x = i % W;
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) {
+      const float* u = fac + (f * R + r) * (fh + fw);
+      const float* h = hor + ((size_t)(f * R + r) * PHh + y) * W + x;
+      for (int t = 0; t < fh; ++t) acc = fmaf(u[t], h[t * W], acc);
+    }
+    Y[((img * out_maps + C + f * C + c) * (int64_t)H + y) * W + x] = acc;
+  }
+}
+
 enum StepKind { ST_GEMM = 0, ST_POOL = 1, ST_COPY = 2, ST_CONTRAST = 3 };
 
 struct Step {
@@ -439,6 +486,7 @@ struct Step {
   float* d_bias = nullptr;
   float* d_fixed = nullptr;     // contrast coefficients (f32)
   int F = 0, fh = 0, fw = 0, out_maps = 0;   // contrast
+  int rank = 0;                 // > 0: separable factors in d_fixed (contrast_sep_kernel)
 };
 
 }  // namespace tc
@@ -461,6 +509,69 @@ namespace ck {
 namespace tc {
 
 static int64_t round_up(int64_t v, int64_t q) { return (v + q - 1) / q * q; }
+
+// Low-rank factors of an fh x fw filter K (row-major, f64): the eigenpairs of
+// K^T K by cyclic Jacobi sweeps give K = sum_r (K v_r) v_r^T over the
+// eigenvectors v_r with non-negligible eigenvalues.  Returns the rank, or 0
+// when the filter is not low-rank enough to pay (or the reconstruction is not
+// within 1e-12 of K's largest entry); factors: per r, u_r (fh) then v_r (fw).
+static int low_rank(const double* K, int fh, int fw, std::vector<double>& fac) {
+  const int n = fw;
+  std::vector<double> A((size_t)n * n, 0.0), V((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    V[i * n + i] = 1.0;
+    for (int j = 0; j < n; ++j)
+      for (int t = 0; t < fh; ++t) A[i * n + j] += K[t * fw + i] * K[t * fw + j];
+  }
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) off += A[p * n + q] * A[p * n + q];
+    if (off < 1e-60) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        if (fabs(A[p * n + q]) < 1e-300) continue;
+        const double th = 0.5 * atan2(2 * A[p * n + q], A[q * n + q] - A[p * n + p]);
+        const double c = cos(th), s = sin(th);
+        for (int k = 0; k < n; ++k) {          // A <- J^T A J, V <- V J
+          const double akp = A[k * n + p], akq = A[k * n + q];
+          A[k * n + p] = c * akp - s * akq;
+          A[k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = A[p * n + k], aqk = A[q * n + k];
+          A[p * n + k] = c * apk - s * aqk;
+          A[q * n + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[k * n + p], vkq = V[k * n + q];
+          V[k * n + p] = c * vkp - s * vkq;
+          V[k * n + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  double kmax = 0.0, lmax = 0.0;
+  for (int i = 0; i < fh * fw; ++i) kmax = std::max(kmax, fabs(K[i]));
+  for (int i = 0; i < n; ++i) lmax = std::max(lmax, A[i * n + i]);
+  fac.clear();
+  int rank = 0;
+  std::vector<double> rec((size_t)fh * fw, 0.0);
+  for (int r = 0; r < n; ++r) {
+    if (A[r * n + r] <= 1e-12 * lmax) continue;   // sigma_r <= 1e-6 sigma_max: noise of K^T K
+    std::vector<double> u(fh, 0.0);
+    for (int t = 0; t < fh; ++t)
+      for (int j = 0; j < fw; ++j) u[t] += K[t * fw + j] * V[j * n + r];
+    for (int t = 0; t < fh; ++t) fac.push_back(u[t]);
+    for (int j = 0; j < fw; ++j) fac.push_back(V[j * n + r]);
+    for (int t = 0; t < fh; ++t)
+      for (int j = 0; j < fw; ++j) rec[t * fw + j] += u[t] * V[j * n + r];
+    ++rank;
+  }
+  double err = 0.0;
+  for (int i = 0; i < fh * fw; ++i) err = std::max(err, fabs(rec[i] - K[i]));
+  if (rank == 0 || err > 1e-12 * kmax || 2 * rank * (fh + fw) * 2 > fh * fw) return 0;
+  return rank;
+}
 
 static int make_gemm(ck_tc_eval* P, Step& st, int S, int H, int W, int kx, int ky, int tx, int ty,
                      int cx, int cy, int N, int OH, int OW, int act, int dst_maps, int dst_off,
@@ -630,6 +741,25 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
       std::vector<float> coef((size_t)st.F * st.fh * st.fw);
       for (size_t j = 0; j < coef.size(); ++j) coef[j] = (float)L.filter_coeffs[j];
       st.smem = sizeof(float) * ((size_t)(H + st.fh - 1) * (W + st.fw - 1 + 4) + coef.size());
+      // low-rank filters (every one of the same rank R): separable passes
+      {
+        std::vector<double> all, f1;
+        int R = -1;
+        for (int f = 0; f < st.F && R != 0; ++f) {
+          const int r = ck::tc::low_rank(L.filter_coeffs + (size_t)f * st.fh * st.fw, st.fh,
+                                         st.fw, f1);
+          R = (R < 0 || R == r) ? r : 0;
+          all.insert(all.end(), f1.begin(), f1.end());
+        }
+        const size_t sm_sep = sizeof(float) * ((size_t)(H + st.fh - 1) * (W + st.fw - 1) +
+                                               (size_t)st.F * std::max(R, 0) * (H + st.fh - 1) * W +
+                                               all.size());
+        if (R > 0 && sm_sep <= 200 * 1024 && !getenv("CKB200_TC_NOSEP")) {
+          st.rank = R;
+          st.smem = sm_sep;
+          coef.assign(all.begin(), all.end());
+        }
+      }
       CK_CHECK(st.smem <= 200 * 1024, CK_E_DIMENSION, "tensor-core eval: contrast window too large");
       if (cudaMalloc(&st.d_fixed, sizeof(float) * coef.size()) != cudaSuccess ||
           cudaMemcpy(st.d_fixed, coef.data(), sizeof(float) * coef.size(),
@@ -691,6 +821,8 @@ int ck_tc_create(const ck_layer_desc* layers, int n_layers, int device, int64_t 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024)) return fail(ck::set_error(CK_E_CUDA, "tensor-core eval: kernel attributes"));
     if (st.kind == ck::tc::ST_CONTRAST)
       if (cudaSuccess != cudaFuncSetAttribute(ck::tc::contrast_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ||
+          cudaSuccess != cudaFuncSetAttribute(ck::tc::contrast_sep_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) return fail(ck::set_error(CK_E_CUDA, "tensor-core eval: kernel attributes"));
   }
 
@@ -750,6 +882,9 @@ int ck_tc_eval_run(ck_tc_eval* P, const uint8_t* images, const float* lut, int64
         const int64_t total = nb * st.maps * (int64_t)st.OH * st.OW;
         ck::tc::pool_kernel<<<ck::blocks_for(total, 256), 256, 0, s>>>(
             X, (int)(nb * st.maps), st.H, st.W, st.px, st.py, st.OH, st.OW, Y);
+      } else if (st.kind == ck::tc::ST_CONTRAST && st.rank > 0) {
+        ck::tc::contrast_sep_kernel<<<(int)(nb * st.maps), 256, st.smem, s>>>(
+            X, st.maps, st.H, st.W, st.d_fixed, st.F, st.rank, st.fh, st.fw, Y, st.out_maps);
       } else if (st.kind == ck::tc::ST_CONTRAST) {
         ck::tc::contrast_kernel<<<(int)(nb * st.maps), 256, st.smem, s>>>(
             X, st.maps, st.H, st.W, st.d_fixed, st.F, st.fh, st.fw, Y, st.out_maps);
