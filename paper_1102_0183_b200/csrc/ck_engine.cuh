@@ -603,6 +603,38 @@ __device__ __forceinline__ void conv_block_smem(float* acc, const float* src, co
   const unsigned s0 = (unsigned)__cvta_generic_to_shared(src);
   const unsigned o0 = (unsigned)__cvta_generic_to_shared(soff);
   const unsigned w0 = (unsigned)__cvta_generic_to_shared(w);
+  if (tx == 1 && ty == 1) {
+    // stride 1: the block's (PB+KY-1) x (PB+KX-1) source window is read one
+    // row at a time into registers and every cell whose kernel row v covers
+    // it takes its taps from there -- (PB+KY-1)(PB+KX-1) loads per source
+    // instead of PB*PB*KX*KY.  A cell's sum still runs k, then v (window rows
+    // ascend), then u: bit-identical.
+    constexpr int WL = PB + KX - 1;
+    for (int k = 0; k < nk; ++k) {
+      const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0 + 4u * k);
+      float wr[KK];
+#pragma unroll
+      for (int t = 0; t < KK; ++t) wr[t] = lds_f32(w0 + 4u * (k * KK + t));
+#pragma unroll
+      for (int row = 0; row < PB + KY - 1; ++row) {
+        float xr[WL];
+#pragma unroll
+        for (int j = 0; j < WL; ++j) xr[j] = lds_f32(sb + 4u * (row * sw + j));
+#pragma unroll
+        for (int cy = 0; cy < PB; ++cy) {
+          const int v = row - cy;
+          if (v < 0 || v >= KY) continue;
+#pragma unroll
+          for (int u = 0; u < KX; ++u)
+#pragma unroll
+            for (int cx = 0; cx < PB; ++cx)
+              acc[cy * PB + cx] =
+                  __fadd_rn(acc[cy * PB + cx], __fmul_rn(wr[v * KX + u], xr[cx + u]));
+        }
+      }
+    }
+    return;
+  }
   for (int k = 0; k < nk; ++k) {
     const unsigned sb = s0 + 4u * (unsigned)lds_s32(o0 + 4u * k);
 #pragma unroll
