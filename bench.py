@@ -462,6 +462,28 @@ def sharded_eval_step(ctx, predict_into, labels, first, mine, pred, gathered, wr
         gathered.copy_(pred)
 
 
+def latency_floor(name, phases, barrier_us, sm_mhz, fadd_cycles=4):
+    """Latency bound of one online step: `phases` dependent team
+    barriers at the measured cost, plus every conv layer's reference-order
+    forward chain (bias, then n_src * kx * ky dependent f32 FADDs per output
+    cell, kernels.py:78-86) at the FADD latency -- work the step cannot
+    parallelise or reorder while staying bit-exact.  Everything else (the
+    backward sums, FC layers, staging) is counted as free."""
+    from paper_1102_0183_b200.configs import spec_for
+    spec = spec_for(name)
+    chain = 0
+    for i, ls in enumerate(spec.layers):
+        if ls.kind == "convolutional":
+            prev = spec.layers[i - 1]
+            fan_in = ls.in_degree if ls.connectivity == "random" else prev.out_maps
+            chain += fan_in * ls.kernel[0] * ls.kernel[1]
+    chain_us = chain * fadd_cycles / (sm_mhz * 1e6) * 1e6
+    return {"us": phases * barrier_us + chain_us, "barriers_us": phases * barrier_us,
+            "conv_chain_steps": chain, "conv_chain_us": chain_us,
+            "model": f"{phases} barriers x {barrier_us:.2f} us + {chain} dependent FADDs x "
+                     f"{fadd_cycles} cycles at {sm_mhz:.0f} MHz"}
+
+
 def _traffic(name, n_img, kind="train"):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(tpath):
@@ -736,12 +758,19 @@ def run_ours(args):
     # phases and their team barriers, not by FLOPs or bytes
     try:
         pw, pb = training.profile_phases(net, train.limit(min(args.imgs_per_step, 500)), ETA)
-        latency = {"phases_per_image": int(len(pw)),
+        live = [i for i in range(len(pw)) if pw[i] > 0 or pb[i] > 0]   # (skipped: prepass)
+        bar_us = float(pb.sum()) / 1e3
+        floor = latency_floor(args.config, len(live), bar_us / max(1, len(live)), sm_nominal)
+        step_us = (float(pw.sum()) + float(pb.sum())) / 1e3
+        latency = {"phases_per_image": len(live),
                    "work_us_per_image": float(pw.sum()) / 1e3,
-                   "barrier_us_per_image": float(pb.sum()) / 1e3,
+                   "barrier_us_per_image": bar_us,
                    "per_phase_us": [round(float(w) / 1e3, 2) for w in pw],
+                   "floor": floor, "frac_of_floor": floor["us"] / step_us if step_us else None,
                    "note": "slowest CTA's work per phase + the team barrier after it "
-                           "(%globaltimer, instrumented launch); the step time is their sum"}
+                           "(%globaltimer, instrumented launch); the step time is their sum. "
+                           "floor: the latency bound of the online step -- its team "
+                           "barriers plus the reference-order conv chains it cannot split"}
     except Exception as exc:          # instrumentation is diagnostic only
         latency = {"error": str(exc)[:200]}
     kind, ctas, threads_per = net.team()
