@@ -974,7 +974,7 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
     // one pool block per thread (many cells per CTA), else one cell per
     // thread on the reference-order chain with padded (v4) weights
     const bool block_path = KX > 0 && wst && (whole || slots) && P.px == P.py && P.px >= 2 &&
-                            P.px <= 4 && n_items > 2 * (int)blockDim.x;
+                            P.px <= 4 && n_items > (int)blockDim.x;
     const bool padw = KX > 0 && wst && (whole || slots) && !block_path;
     const int nw = (k1 - k0) * (padw ? KKP : kk) + d1 + 1 - d0;
     int* soff = reinterpret_cast<int*>(tm.smem + used);
