@@ -64,8 +64,10 @@ struct ClusterTeam {
 // Grid team barrier: a monotonic arrival counter (zeroed before each launch).
 // Each CTA's thread 0 adds 1 with release semantics (cumulative over the
 // CTA's writes, ordered before it by bar.sync) and polls with acquire until
-// every CTA of this barrier generation has arrived.  No reset, no return
-// value on the arrival, no full fences.
+// every CTA of this barrier generation has arrived.  No reset, no full
+// fences.  The arrival returns the old count, so the last CTA to arrive
+// skips the poll (tools/mb_barrier.cu: 2300 vs 2600 cycles per barrier with
+// 2 KB of stores per CTA to release; ~1.1 us is two L2 round trips).
 struct GridTeam {
   __device__ static unsigned rank(int ctas) { return blockIdx.x % ctas; }
   __device__ static unsigned index(int ctas) { return blockIdx.x / ctas; }
@@ -73,8 +75,11 @@ struct GridTeam {
     __syncthreads();
     if (threadIdx.x == 0) {
       target += (unsigned)ctas;
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(R.bar) : "memory");
-      while ((int)(ld_acquire(R.bar) - target) < 0) {
+      unsigned old;
+      asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(R.bar) : "memory");
+      if (old + 1 != target) {
+        while ((int)(ld_acquire(R.bar) - target) < 0) {
+        }
       }
     }
     __syncthreads();

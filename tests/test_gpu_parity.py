@@ -436,15 +436,34 @@ def test_specialised_kernels_bit_identical_to_generic(name):
     slow.close()
 
 
-def test_contrast_prepass_bit_identical():
+PREPASS_NETS = {
+    "C3": None,
+    "hat5_sobel": "input 2x16x16; imgproc hat5,sobel; conv 4M k5x5 s0x0 rand3; maxpool 3x3; "
+                  "fc 6N; output 4",
+    "odd": "input 1x15x15; imgproc hat3; conv 3M k3x3 s0x0; maxpool 2x2; fc 5N; output 3",
+}
+
+
+@pytest.mark.parametrize("name", list(PREPASS_NETS))
+@pytest.mark.parametrize("kernel", ["strip", "lanes"])
+def test_contrast_prepass_bit_identical(name, kernel):
     """Training launches of nets with an image-processing layer compute it for
-    every visited image in a batched prepass (ck_net.cu contrast_pre_kernel)
-    and skip the per-image phase 0; the result must equal the per-image path
-    bit for bit (CKB200_NO_PRE=1 disables the prepass)."""
+    every visited image in a batched prepass (ck_net.cu: the strip kernel, or
+    the lane kernel with CKB200_PRE_LANES=1) and skip the per-image phase 0;
+    the result must equal the per-image path bit for bit (CKB200_NO_PRE=1
+    disables the prepass)."""
     import os
+    import warnings
     from paper_1102_0183_b200.configs import spec_for
-    spec = spec_for("C3")
-    data = ck.make_glyph_dataset(6, spec.n_classes, 48, seed=8, channels=2)
+    if PREPASS_NETS[name] is None:
+        spec = spec_for(name)
+    else:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            spec = ck.parse_architecture(PREPASS_NETS[name])
+    first = spec.layers[0]
+    data = ck.make_glyph_dataset(6, spec.n_classes, first.out_width, seed=8,
+                                 channels=first.out_maps)
     cfg = ck.TrainConfig(epochs=1, eta0=1e-3, seed=2)
     a = ck.NetworkState(spec, 3)
     b = ck.NetworkState(spec, 3)
@@ -453,7 +472,12 @@ def test_contrast_prepass_bit_identical():
         m_b = ck.train_epoch(b, data, cfg, 0)
     finally:
         del os.environ["CKB200_NO_PRE"]
-    m_a = ck.train_epoch(a, data, cfg, 0)
+    if kernel == "lanes":
+        os.environ["CKB200_PRE_LANES"] = "1"
+    try:
+        m_a = ck.train_epoch(a, data, cfg, 0)
+    finally:
+        os.environ.pop("CKB200_PRE_LANES", None)
     assert m_a == m_b
     np.testing.assert_array_equal(a.flat_parameters(), b.flat_parameters())
     a.close()
