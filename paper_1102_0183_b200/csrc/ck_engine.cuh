@@ -418,6 +418,76 @@ __device__ __forceinline__ double contrast_cell(const LayerDev& L, const float* 
   return acc;
 }
 
+// The contrast layer laid out for the f64 pipe, same bits as contrast_cell:
+// a thread takes a strip of kStrip adjacent cells of one (filter, row) and
+// computes contrast_cell's eight lane partials itself (rows i = s mod 8, fma
+// chains along the row, 4 cells at a time with a sliding register window over
+// a replicated-border f64 window of the channel), then combines them in the
+// xor tree's order ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7)).  ~0.5 shared loads
+// per fma instead of two clamps, a convert and two loads per tap.
+constexpr int kStrip = 4;
+static_assert(kImgLanes == 8, "contrast_strips restates the 8-lane xor tree");
+
+__host__ __device__ __forceinline__ int strip_pitch(const LayerDev& L) { return L.w + L.fw + kStrip; }
+
+__device__ __forceinline__ void strip_partial(const double* win, int PW, const double* k, int fh,
+                                              int fw, int y, int s, double (&p)[kStrip]) {
+#pragma unroll
+  for (int c = 0; c < kStrip; ++c) p[c] = 0.0;
+  for (int i = s; i < fh; i += kImgLanes) {
+    const double* row = win + (y + i) * PW;
+    const double* kr = k + i * fw;
+    double x0 = row[0], x1 = row[1], x2 = row[2], x3 = row[3];
+#pragma unroll 4
+    for (int j = 0; j < fw; ++j) {
+      const double w = kr[j];
+      p[0] = fma(w, x0, p[0]);
+      p[1] = fma(w, x1, p[1]);
+      p[2] = fma(w, x2, p[2]);
+      p[3] = fma(w, x3, p[3]);
+      x0 = x1;
+      x1 = x2;
+      x2 = x3;
+      x3 = row[j + 4];
+    }
+  }
+}
+
+// The responses of channel c (every filter) from its window `win` ((h + fh -
+// 1) rows of strip_pitch(L) doubles: win[r][q] = x[clamp(r - fh/2)][clamp(q -
+// fw/2)]) and the f64 filters `kf`, into the layer's y `o`; this CTA's threads.
+__device__ __forceinline__ void contrast_strips(const LayerDev& L, const double* win,
+                                                const double* kf, int c, float* o) {
+  const int C = L.src_maps, H = L.h, W = L.w, hw = H * W;
+  const int fh = L.fh, fw = L.fw, PW = strip_pitch(L);
+  const int F = (L.cells - C * hw) / (C * hw);
+  const int sx = (W + kStrip - 1) / kStrip;
+  for (int job = threadIdx.x; job < F * H * sx; job += blockDim.x) {
+    const int f = job / (H * sx), y = (job / sx) % H, x0 = (job % sx) * kStrip;
+    const double* k = kf + f * fh * fw;
+    const double* w0 = win + x0;
+    double a[kStrip], b[kStrip], p[kStrip], q[kStrip];
+    strip_partial(w0, PW, k, fh, fw, y, 0, p);   // B0 = (p0 + p4) + (p2 + p6)
+    strip_partial(w0, PW, k, fh, fw, y, 4, q);
+#pragma unroll
+    for (int e = 0; e < kStrip; ++e) a[e] = p[e] + q[e];
+    strip_partial(w0, PW, k, fh, fw, y, 2, p);
+    strip_partial(w0, PW, k, fh, fw, y, 6, q);
+#pragma unroll
+    for (int e = 0; e < kStrip; ++e) b[e] = a[e] + (p[e] + q[e]);
+    strip_partial(w0, PW, k, fh, fw, y, 1, p);   // B1 = (p1 + p5) + (p3 + p7)
+    strip_partial(w0, PW, k, fh, fw, y, 5, q);
+#pragma unroll
+    for (int e = 0; e < kStrip; ++e) a[e] = p[e] + q[e];
+    strip_partial(w0, PW, k, fh, fw, y, 3, p);
+    strip_partial(w0, PW, k, fh, fw, y, 7, q);
+    float* orow = o + ((int64_t)(C + f * C + c) * H + y) * W;
+#pragma unroll
+    for (int e = 0; e < kStrip; ++e)
+      if (x0 + e < W) orow[x0 + e] = (float)(b[e] + (a[e] + (p[e] + q[e])));
+  }
+}
+
 // correlate(mode="nearest") per (filter, channel): f64 sum, one rounding.
 __device__ __forceinline__ void op_imgproc(const NetGeo& N, const NetPtr& R, const LayerDev& L, float* act,
                                            const TeamCtx& tm) {
@@ -431,6 +501,30 @@ __device__ __forceinline__ void op_imgproc(const NetGeo& N, const NetPtr& R, con
   float* out = act + L.y_off;
   const int hw = L.h * L.w;
   const int C = I.maps;
+  if (tm.size == 1) {
+    // one CTA per image (evaluation): the strip form, channel by channel
+    const int PH = L.h + L.fh - 1, PW = strip_pitch(L);
+    const int nf = (L.cells - C * hw) / (C * hw) * L.fh * L.fw;
+    const int u = (used + 1) & ~1;   // 8-byte alignment for the doubles
+    if (u + 2 * (nf + PH * PW) <= tm.smem_floats) {
+      double* kf = reinterpret_cast<double*>(tm.smem + u);
+      double* win = kf + nf;
+      for (int i = threadIdx.x; i < nf; i += blockDim.x) kf[i] = __ldg(R.filt + L.o_filt + i);
+      stage_sync();
+      for (int q = threadIdx.x; q < C * hw; q += blockDim.x) out[q] = src[q];
+      const int cy = L.fh / 2, cx = L.fw / 2;
+      for (int c = 0; c < C; ++c) {
+        for (int i = threadIdx.x; i < PH * PW; i += blockDim.x) {
+          const int r = min(max(i / PW - cy, 0), L.h - 1), q = min(max(i % PW - cx, 0), L.w - 1);
+          win[i] = (double)src[c * hw + r * L.w + q];
+        }
+        __syncthreads();
+        contrast_strips(L, win, kf, c, out);
+        __syncthreads();
+      }
+      return;
+    }
+  }
   const int cy = L.fh / 2, cx = L.fw / 2;
   const int taps = L.fh * L.fw;
   const int lane = lane_id();

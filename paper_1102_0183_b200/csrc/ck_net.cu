@@ -837,40 +837,10 @@ contrast_pre_kernel(LayerDev L, const double* __restrict__ filt, const uint8_t* 
   }
 }
 
-// The same layer, same bits, laid out for the f64 pipe: one CTA per (visit,
-// channel), the channel staged once as f64 with its replicated border, every
-// thread a strip of kPreStrip adjacent cells of one filter.  contrast_cell's
-// eight lane partials (rows i = s mod 8, fma chains along the row) are
-// computed here by one thread, 4 cells at a time with a sliding register
-// window over the row, and combined in the xor tree's order
-// ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7)) -- bit-identical, ~0.5 shared loads
-// per fma instead of a clamp, a convert and two loads per tap.
-constexpr int kPreStrip = 4;
+// The same layer, same bits, laid out for the f64 pipe (contrast_strips,
+// ck_engine.cuh): one CTA per (visit, channel), the channel staged once as
+// f64 with its replicated border.
 constexpr int kPreThreads = 288;
-static_assert(kImgLanes == 8, "contrast_pre_strip_kernel restates the 8-lane tree");
-
-__device__ __forceinline__ void pre_partial(const double* win, int PW, const double* k, int fh,
-                                            int fw, int y, int s, double (&p)[kPreStrip]) {
-#pragma unroll
-  for (int c = 0; c < kPreStrip; ++c) p[c] = 0.0;
-  for (int i = s; i < fh; i += kImgLanes) {
-    const double* row = win + (y + i) * PW;
-    const double* kr = k + i * fw;
-    double x0 = row[0], x1 = row[1], x2 = row[2], x3 = row[3];
-#pragma unroll 4
-    for (int j = 0; j < fw; ++j) {
-      const double w = kr[j];
-      p[0] = fma(w, x0, p[0]);
-      p[1] = fma(w, x1, p[1]);
-      p[2] = fma(w, x2, p[2]);
-      p[3] = fma(w, x3, p[3]);
-      x0 = x1;
-      x1 = x2;
-      x2 = x3;
-      x3 = row[j + 4];
-    }
-  }
-}
 
 __global__ void __launch_bounds__(kPreThreads)
 contrast_pre_strip_kernel(LayerDev L, const double* __restrict__ filt, const uint8_t* images,
@@ -880,7 +850,7 @@ contrast_pre_strip_kernel(LayerDev L, const double* __restrict__ filt, const uin
   const int C = L.src_maps, H = L.h, W = L.w, hw = H * W;
   const int fh = L.fh, fw = L.fw, cy = fh / 2, cx = fw / 2;
   const int F = (L.cells - C * hw) / (C * hw);
-  const int PW = W + fw + kPreStrip, PH = H + fh - 1;
+  const int PW = strip_pitch(L), PH = H + fh - 1;
   double* win = dsm;                          // PH x PW, replicated border
   double* kf = dsm + (size_t)PH * PW;         // F x fh x fw
   const int64_t t = blockIdx.x / C;
@@ -899,33 +869,7 @@ contrast_pre_strip_kernel(LayerDev L, const double* __restrict__ filt, const uin
   }
   for (int i = threadIdx.x; i < F * fh * fw; i += blockDim.x) kf[i] = __ldg(filt + L.o_filt + i);
   __syncthreads();
-  const int sx = (W + kPreStrip - 1) / kPreStrip;
-  for (int job = threadIdx.x; job < F * H * sx; job += blockDim.x) {
-    const int f = job / (H * sx), y = (job / sx) % H, x0 = (job % sx) * kPreStrip;
-    const double* k = kf + f * fh * fw;
-    const double* w0 = win + x0;
-    double a[kPreStrip], b[kPreStrip], p[kPreStrip], q[kPreStrip];
-    // B0 = (p0 + p4) + (p2 + p6)
-    pre_partial(w0, PW, k, fh, fw, y, 0, p);
-    pre_partial(w0, PW, k, fh, fw, y, 4, q);
-#pragma unroll
-    for (int e = 0; e < kPreStrip; ++e) a[e] = p[e] + q[e];
-    pre_partial(w0, PW, k, fh, fw, y, 2, p);
-    pre_partial(w0, PW, k, fh, fw, y, 6, q);
-#pragma unroll
-    for (int e = 0; e < kPreStrip; ++e) b[e] = a[e] + (p[e] + q[e]);
-    // B1 = (p1 + p5) + (p3 + p7)
-    pre_partial(w0, PW, k, fh, fw, y, 1, p);
-    pre_partial(w0, PW, k, fh, fw, y, 5, q);
-#pragma unroll
-    for (int e = 0; e < kPreStrip; ++e) a[e] = p[e] + q[e];
-    pre_partial(w0, PW, k, fh, fw, y, 3, p);
-    pre_partial(w0, PW, k, fh, fw, y, 7, q);
-    float* orow = o + ((int64_t)(C + f * C + c) * H + y) * W;
-#pragma unroll
-    for (int e = 0; e < kPreStrip; ++e)
-      if (x0 + e < W) orow[x0 + e] = (float)(b[e] + (a[e] + (p[e] + q[e])));
-  }
+  contrast_strips(L, win, kf, c, o);
 }
 
 // The prepass for a training launch over `n` visits (nullptr in *pre when the
@@ -954,7 +898,7 @@ int run_prepass(ck_net* net, const uint8_t* images, const float* lut, const int3
   }
   const LayerDev& I = N.L[1];
   const int n_filt = (I.cells - I.src_maps * I.h * I.w) / (I.src_maps * I.h * I.w);
-  const size_t strip_smem = sizeof(double) * ((size_t)(I.h + I.fh - 1) * (I.w + I.fw + kPreStrip) +
+  const size_t strip_smem = sizeof(double) * ((size_t)(I.h + I.fh - 1) * strip_pitch(I) +
                                               (size_t)n_filt * I.fh * I.fw);
   if (strip_smem <= 200 * 1024 && !getenv("CKB200_PRE_LANES")) {
     contrast_pre_strip_kernel<<<(unsigned)(n * I.src_maps), kPreThreads, strip_smem, st>>>(
