@@ -1556,13 +1556,15 @@ __device__ __forceinline__ void emit_wg(int o, int t, double sum, double* out, f
 // across pooled rows the winners' rows already ascend, inside one the
 // columns ascend with the pooled column -- so the adds follow the
 // reference's (y, x) order exactly.  Bit-identical to kernels.pull_bwd.
-// Every CTA takes a contiguous range of source cells; the winners of all
-// dest maps and the CTA's backward entries' (old) kernels are staged.
+// Every CTA takes a contiguous range of source cells; its backward entries'
+// (old) kernels and dest indices are staged, and the winners either of every
+// dest map (ed: entry -> dest map slot) or, when that is less, a copy per
+// backward entry (ed == nullptr: slot = entry).
 template <int PRM, int PCM>
 __device__ __forceinline__ void pull_gather_cells(const NetGeo& N, const NetPtr& R,
                                                   const LayerDev& L, float* act, Span cs,
                                                   const int* wr, const float* wdv,
-                                                  const float* ws, int ka) {
+                                                  const float* ws, const int* ed, int ka) {
   const int li = &L - N.L;
   const LayerDev& S = N.L[li - 1];
   const LayerDev& P = N.L[li + 1];
@@ -1571,6 +1573,7 @@ __device__ __forceinline__ void pull_gather_cells(const NetGeo& N, const NetPtr&
   const unsigned wr0 = (unsigned)__cvta_generic_to_shared(wr);
   const unsigned wd0 = (unsigned)__cvta_generic_to_shared(wdv);
   const unsigned ws0 = (unsigned)__cvta_generic_to_shared(ws);
+  const unsigned ed0 = ed ? (unsigned)__cvta_generic_to_shared(ed) : 0u;
   for (int cell = cs.b + threadIdx.x; cell < cs.e; cell += blockDim.x) {
     const int s = cell / shw, pix = cell - s * shw;
     const int j = pix / S.w, i = pix - j * S.w;
@@ -1594,9 +1597,9 @@ __device__ __forceinline__ void pull_gather_cells(const NetGeo& N, const NetPtr&
       const int tap0 = j * L.kx + i;     // tap = tap0 - r*ty*kx - c*tx
 #pragma unroll 2
       for (int e = e0; e < e1; ++e) {
-        const int d = t_bwd_dst(R, L, e);
-        const unsigned wrd = wr0 + 4u * (unsigned)(d * phw);
-        const unsigned wdd = wd0 + 4u * (unsigned)(d * phw);
+        const int slot = ed ? lds_s32(ed0 + 4u * (unsigned)(e - ka)) : e - ka;
+        const unsigned wrd = wr0 + 4u * (unsigned)(slot * phw);
+        const unsigned wdd = wd0 + 4u * (unsigned)(slot * phw);
         const unsigned wb = ws0 + 4u * (unsigned)((e - ka) * kk);
         int key[PRM][PCM];
         double term[PRM][PCM];
@@ -1652,6 +1655,45 @@ __device__ __forceinline__ void conv_pull_gather(const NetGeo& N, const NetPtr& 
   if (cs.b >= cs.e) return;                      // uniform per CTA
   CK_SUBT(tm, 16);
   const int nwin = L.maps * phw;
+  const int prm = ((L.ky - 1) / L.ty + P.py - 1) / P.py + 1;
+  const int pcm = ((L.kx - 1) / L.tx + P.px - 1) / P.px + 1;
+  auto run = [&](Span ch, const int* wr, const float* wdv, const float* ws, const int* ed,
+                 int ka) {
+    if (prm <= 1 && pcm <= 1) pull_gather_cells<1, 1>(N, R, L, act, ch, wr, wdv, ws, ed, ka);
+    else if (prm <= 2 && pcm <= 2) pull_gather_cells<2, 2>(N, R, L, act, ch, wr, wdv, ws, ed, ka);
+    else if (prm <= 3 && pcm <= 3) pull_gather_cells<3, 3>(N, R, L, act, ch, wr, wdv, ws, ed, ka);
+    else pull_gather_cells<5, 5>(N, R, L, act, ch, wr, wdv, ws, ed, ka);
+  };
+  // sparse tables: the winners of just this CTA's entries' dest maps (a copy
+  // per entry) when that stages less than every dest map's and fits at once
+  {
+    const int ka = t_bwd_off(R, L, cs.b / shw), kb = t_bwd_off(R, L, (cs.e - 1) / shw + 1);
+    const int ne = kb - ka, nwe = ((ne * phw + 3) & ~3);
+    if (ne * phw < nwin && 2 * nwe + ((ne * kk + 3) & ~3) <= tm.smem_floats) {
+      int* wr = reinterpret_cast<int*>(tm.smem);
+      float* wdv = tm.smem + nwe;
+      float* ws = wdv + nwe;
+      const int* wrc_g = reinterpret_cast<const int*>(act + P.wrc_off);
+      const float* wd_g = act + P.wd_off;
+      for (int i = threadIdx.x; i < ne * phw; i += blockDim.x) {
+        const int q = i / phw;
+        const int from = t_bwd_dst(R, L, ka + q) * phw + (i - q * phw);
+        cp_async4(wr + i, wrc_g + from);
+        cp_async4(wdv + i, wd_g + from);
+      }
+      for (int e = threadIdx.x; e < ne * kk; e += blockDim.x) {
+        const int q = e / kk;
+        cp_async4(ws + e, arena + t_bwd_widx(R, L, ka + q) + (e - q * kk));
+      }
+      stage_sync();
+      CK_SUBT(tm, 17);
+      run(cs, wr, wdv, ws, nullptr, ka);
+      CK_SUBT(tm, 18);
+      __syncthreads();
+      CK_SUBT(tm, 19);
+      return;
+    }
+  }
   // the host sets pullg only when the winners of all dest maps and any CTA's
   // backward-entry kernels fit the scratch (ck_net.cu); chunks of cells keep
   // the kernels' share bounded for wide backward lists
@@ -1661,30 +1703,26 @@ __device__ __forceinline__ void conv_pull_gather(const NetGeo& N, const NetPtr& 
   const float* wdv = stage(act + P.wd_off, nwin, tm, used);
   float* ws = tm.smem + used;
   const int cap = tm.smem_floats - used;
-  const int prm = ((L.ky - 1) / L.ty + P.py - 1) / P.py + 1;
-  const int pcm = ((L.kx - 1) / L.tx + P.px - 1) / P.px + 1;
   for (int c0 = cs.b; c0 < cs.e;) {
-    // cells [c0, c1): whole source maps' backward entries must fit
+    // cells [c0, c1): whole source maps' backward entries (kernel + dest) must fit
     int c1 = cs.e;
     int m0 = c0 / shw, m1 = (c1 - 1) / shw;
     int ka = t_bwd_off(R, L, m0), kb = t_bwd_off(R, L, m1 + 1);
-    while ((kb - ka) * kk > cap && m1 > m0) {
+    while ((kb - ka) * (kk + 1) + 4 > cap && m1 > m0) {
       c1 = m1 * shw;
       m1 = (c1 - 1) / shw;
       kb = t_bwd_off(R, L, m1 + 1);
     }
     if (c0 != cs.b) __syncthreads();             // previous chunk's kernels consumed
+    int* ed = reinterpret_cast<int*>(ws + (((kb - ka) * kk + 3) & ~3));
     for (int e = threadIdx.x; e < (kb - ka) * kk; e += blockDim.x) {
       const int q = e / kk;
       cp_async4(ws + e, arena + t_bwd_widx(R, L, ka + q) + (e - q * kk));
     }
+    for (int e = threadIdx.x; e < kb - ka; e += blockDim.x) ed[e] = t_bwd_dst(R, L, ka + e);
     stage_sync();
     CK_SUBT(tm, 17);
-    const Span ch{c0, c1};
-    if (prm <= 1 && pcm <= 1) pull_gather_cells<1, 1>(N, R, L, act, ch, wr, wdv, ws, ka);
-    else if (prm <= 2 && pcm <= 2) pull_gather_cells<2, 2>(N, R, L, act, ch, wr, wdv, ws, ka);
-    else if (prm <= 3 && pcm <= 3) pull_gather_cells<3, 3>(N, R, L, act, ch, wr, wdv, ws, ka);
-    else pull_gather_cells<5, 5>(N, R, L, act, ch, wr, wdv, ws, ka);
+    run(Span{c0, c1}, wr, wdv, ws, ed, ka);
     c0 = c1;
   }
   CK_SUBT(tm, 18);

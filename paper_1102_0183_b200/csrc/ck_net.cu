@@ -674,7 +674,7 @@ int build_net_geometry(const ck_layer_desc* layers, int n_layers, NetGeo* geo,
       const char* pm = getenv("CKB200_PULL");
       const bool forced = pm && strcmp(pm, "gather") == 0;
       if ((widest < 128 && D.kx * D.ky > 4 && !forced) ||
-          2 * ((L.maps * phw + 3) & ~3) + widest * D.kx * D.ky > kTeamStageFloats)
+          2 * ((L.maps * phw + 3) & ~3) + widest * (D.kx * D.ky + 1) + 4 > kTeamStageFloats)
         N.L[k].pullg = 0;
     }
     // backward CSR = exact transpose, destinations ascending (topology.invert_table)
