@@ -1268,7 +1268,21 @@ __device__ __forceinline__ void op_fc_fwd(const NetGeo& N, const NetPtr& R, cons
                                           const TeamCtx& tm) {
   const LayerDev& S = N.L[&L - N.L - 1];
   const int n_in = S.cells, n_out = L.cells;
-  const int n_tiles = (n_out + kFcTile - 1) / kFcTile;
+  // tile width: a team with at least two columns per CTA spreads them over
+  // all its CTAs (fewer weights staged per CTA; 4-column tiles of 16-byte row
+  // pieces when the layout allows): C3 / C4 +1%, while narrower layers (C1 /
+  // C2: 150 columns) measured faster with kFcTile, as is one CTA
+  // (evaluation).  The slices fix the bits, not the tile.
+  int tw = kFcTile;
+  bool v4 = false;
+  if (tm.size > 1 && n_out >= 2 * tm.size) {
+    tw = min(kFcTile, (n_out + tm.size - 1) / tm.size);
+    if (n_out % 4 == 0 && (reinterpret_cast<uintptr_t>(R.params + L.p_off) & 15) == 0) {
+      tw = min(kFcTile, (tw + 3) & ~3);
+      v4 = true;
+    }
+  }
+  const int n_tiles = (n_out + tw - 1) / tw;
   if (tm.rank >= n_tiles) return;
   int used = 0;
   const float* x = stage(layer_y(S, act, tm), n_in, tm, used);
@@ -1277,12 +1291,18 @@ __device__ __forceinline__ void op_fc_fwd(const NetGeo& N, const NetPtr& R, cons
   float* out_a = tm.smem + used;
   used += kFcTile;
   const float* W = R.params + L.p_off;
-  const bool wst = used + n_in * kFcTile <= tm.smem_floats;
+  const bool wst = used + n_in * tw <= tm.smem_floats;
   float* wt = tm.smem + used;
   for (int tile = tm.rank; tile < n_tiles; tile += tm.size) {
-    const int j0 = tile * kFcTile;
-    const int nc = min(kFcTile, n_out - j0);
-    if (wst) {
+    const int j0 = tile * tw;
+    const int nc = min(tw, n_out - j0);
+    if (wst && v4) {
+      const int q4 = nc >> 2;   // 16-byte pieces per row (j0, n_out multiples of 4)
+      for (int e = threadIdx.x; e < n_in * q4; e += blockDim.x) {
+        const int i = e / q4, q = e - i * q4;
+        cp_async16(wt + i * nc + 4 * q, W + (int64_t)i * n_out + j0 + 4 * q);
+      }
+    } else if (wst) {
       if (nc == kFcTile) {
         for (int e = threadIdx.x; e < n_in * kFcTile; e += blockDim.x)
           cp_async4(wt + e, W + (e / kFcTile) * n_out + j0 + e % kFcTile);
