@@ -19,7 +19,9 @@ namespace ck {
 constexpr double kActScale = 1.7159;
 constexpr double kActGain = 0.6666;
 
-__device__ __forceinline__ float conv_act(float a) {
+// (one out-of-line copy: the f64 tanh is ~100 instructions, and the
+// training kernel's per-image code footprint is instruction-cache bound)
+static __device__ __noinline__ float conv_act(float a) {
   return (float)(kActScale * tanh(kActGain * (double)a));
 }
 
@@ -27,7 +29,7 @@ __device__ __forceinline__ float conv_act(float a) {
 // rounded in a third of the cases); the device uses CUDA's tanhf (<= 2 ulp).
 // Stated tolerance: a few ulp on FC activations and on every delta (the conv
 // activation, which must be bit-exact, keeps the reference's f64 tanh).
-__device__ __forceinline__ float tanh32(float z) { return tanhf(z); }
+static __device__ __noinline__ float tanh32(float z) { return tanhf(z); }
 
 __device__ __forceinline__ float fc_act(float a) {
   return __fmul_rn((float)kActScale, tanh32(__fmul_rn((float)kActGain, a)));
