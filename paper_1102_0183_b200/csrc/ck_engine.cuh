@@ -1127,11 +1127,12 @@ __device__ __forceinline__ void conv_pool_fwd(const NetGeo& N, const NetPtr& R, 
           if (pooled_only) {
             for (int t = 1; t < blk; ++t)
               if (acc[t] > acc[bt]) bt = t;
-            best = conv_act(acc[bt]);
+            // (one CTA per image -- evaluation -- inlines: acc[] is live)
+            best = tm.size == 1 ? conv_act_inl(acc[bt]) : conv_act(acc[bt]);
           } else {
             for (int t = 0; t < blk; ++t) {   // scan order: rows, then columns
               const int cell = d * hw + (r0 + t / P.px) * L.w + c0 + t % P.px;
-              const float yv = conv_act(acc[t]);
+              const float yv = tm.size == 1 ? conv_act_inl(acc[t]) : conv_act(acc[t]);
               a[cell] = acc[t];
               y[cell] = yv;
               if (zero) dl[cell] = 0.0f;

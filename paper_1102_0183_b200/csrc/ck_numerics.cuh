@@ -20,10 +20,13 @@ constexpr double kActScale = 1.7159;
 constexpr double kActGain = 0.6666;
 
 // (one out-of-line copy: the f64 tanh is ~100 instructions, and the
-// training kernel's per-image code footprint is instruction-cache bound)
-static __device__ __noinline__ float conv_act(float a) {
+// training kernel's per-image code footprint is instruction-cache bound;
+// conv_act_inl for the per-pool-block loops, where a call costs register
+// saves)
+__device__ __forceinline__ float conv_act_inl(float a) {
   return (float)(kActScale * tanh(kActGain * (double)a));
 }
+static __device__ __noinline__ float conv_act(float a) { return conv_act_inl(a); }
 
 // numpy's float32 tanh is a SIMD approximation (~1 ulp from correctly
 // rounded in a third of the cases); the device uses CUDA's tanhf (<= 2 ulp).
