@@ -1949,6 +1949,27 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
             wdd = wd_g + d * phw;
           }
           const float wt = on ? wk[t] : 0.0f;
+          if (fits) {
+            // everything in shared memory: 32-bit shared addresses, no
+            // generic loads / stores in the read-modify-write chain
+            const unsigned a0 = (unsigned)__cvta_generic_to_shared(acc);
+            const unsigned r0 = (unsigned)__cvta_generic_to_shared(wr);
+            const unsigned d0 = (unsigned)__cvta_generic_to_shared(wdd);
+            for (int q0 = 0; q0 < phw; q0 += G) {
+              const int q = q0 + grp;
+              if (on && q < phw) {
+                const int rc = lds_s32(r0 + 4u * q);
+                const unsigned at =
+                    a0 + 8u * (unsigned)((rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx);
+                double v;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(at) : "memory");
+                v += (double)__fmul_rn(lds_f32(d0 + 4u * q), wt);
+                asm volatile("st.shared.f64 [%0], %1;" ::"r"(at), "d"(v) : "memory");
+              }
+              __syncwarp();
+            }
+            continue;
+          }
           for (int q0 = 0; q0 < phw; q0 += G) {   // uniform rounds: group grp takes q0 + grp
             const int q = q0 + grp;
             if (on && q < phw) {
