@@ -1842,10 +1842,23 @@ __device__ __forceinline__ void conv_bwd_sparse(const NetGeo& N, const NetPtr& R
       for (int t = (kk <= 32 ? lane % kk : lane); t < kk; t += (kk <= 32 ? kk : 32)) {
         const float* sv = sp + (t / L.kx) * S.w + t % L.kx;
         double part = 0.0;
+        if (fits) {   // all staged: 32-bit shared addresses
+          const unsigned r0 = (unsigned)__cvta_generic_to_shared(wrp);
+          const unsigned d0 = (unsigned)__cvta_generic_to_shared(wdp);
+          const unsigned s0 = (unsigned)__cvta_generic_to_shared(sv);
 #pragma unroll 4
-        for (int wq = wb; wq < we; ++wq) {
-          const int rc = wrp[wq];
-          part += (double)__fmul_rn(wdp[wq], sv[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx]);
+          for (int wq = wb; wq < we; ++wq) {
+            const int rc = lds_s32(r0 + 4u * wq);
+            part += (double)__fmul_rn(
+                lds_f32(d0 + 4u * wq),
+                lds_f32(s0 + 4u * (unsigned)((rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx)));
+          }
+        } else {
+#pragma unroll 4
+          for (int wq = wb; wq < we; ++wq) {
+            const int rc = wrp[wq];
+            part += (double)__fmul_rn(wdp[wq], sv[(rc >> 16) * L.ty * S.w + (rc & 0xffff) * L.tx]);
+          }
         }
         emit_wg(o, t, part, parts ? parts + task * kk : nullptr, arena, g, upd, eta_f);
       }
